@@ -1,0 +1,38 @@
+"""approxrv-b200: B200-native hot path of approxrv (arXiv 2012.09715).
+
+Approximate Gaussian / non-central chi-squared random variables from cheap
+piecewise inverse-CDF tables, fused with PCG32 generation, and the nested
+multilevel Monte Carlo path kernels that consume them -- hand-written sm_100a
+CUDA behind the C ABI in include/approxrv_b200.h, with the reference's
+Python API (approxrv) mirrored on top.
+"""
+
+__version__ = "0.1.0"
+
+from . import _native  # noqa: F401  (loads libarv_b200.so; fails loudly)
+from ._backend import backend_name, get_kernels
+from .errors import (
+    ApproxRvError, BadMagicError, ChecksumError, ConfigError, DeviceError, DomainError,
+    NumericalError, TableIOError, TruncatedFileError, VersionError,
+)
+from .mlmc import (
+    Allocation, CirParams, GbmParams, LevelSpec, LevelStats, estimate_level, estimate_level_suite,
+    level_stream, optimal_allocation, optimal_allocation_nested, simulate, speedup_report,
+)
+from .sampler import (
+    CoupledGaussianBatch, Pcg32Stream, dyadic_index, eval_constant, eval_dyadic, eval_ncchi2,
+    eval_subdyadic, evaluate, gaussian_inv_cdf, sample_coupled, shard_range,
+)
+from .tables import ConstantTable, DyadicPolyTable, NcChi2Table, SubDyadicTable, load_table, shipped_names
+
+__all__ = [
+    "ApproxRvError", "BadMagicError", "ChecksumError", "ConfigError", "DeviceError", "DomainError",
+    "NumericalError", "TableIOError", "TruncatedFileError", "VersionError",
+    "Allocation", "CirParams", "GbmParams", "LevelSpec", "LevelStats", "estimate_level",
+    "estimate_level_suite", "level_stream", "optimal_allocation", "optimal_allocation_nested",
+    "simulate", "speedup_report",
+    "CoupledGaussianBatch", "Pcg32Stream", "dyadic_index", "eval_constant", "eval_dyadic", "eval_ncchi2",
+    "eval_subdyadic", "evaluate", "gaussian_inv_cdf", "sample_coupled", "shard_range",
+    "ConstantTable", "DyadicPolyTable", "NcChi2Table", "SubDyadicTable", "load_table", "shipped_names",
+    "backend_name", "get_kernels",
+]

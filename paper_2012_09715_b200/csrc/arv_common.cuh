@@ -1,0 +1,199 @@
+// Shared device helpers: PCG32 (state in registers, affine jump-ahead),
+// the integer-domain uniform mapping, the AS241 rational, launch helpers and
+// the per-thread error slot behind arv_last_error().
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "approxrv_b200.h"
+
+namespace arv {
+
+constexpr uint64_t kPcgMult = 6364136223846793005ULL;
+constexpr int kNumSMs = 148;  // B200; the launcher queries the device anyway
+
+// ---------------------------------------------------------------- errors --
+int set_error(int code, const char *fmt, ...);
+int check_launch(const char *what);
+void note_launch(int n = 1);
+int device_sm_count();
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ----------------------------------------------------------------- PCG32 --
+struct Affine {
+    uint64_t a, c;  // s -> a*s + c (mod 2^64)
+};
+
+// Jump-ahead of the LCG s' = M s + inc by `delta` steps (square-and-multiply
+// on the affine map; O(log delta)).
+__host__ __device__ inline Affine lcg_jump(uint64_t delta, uint64_t inc) {
+    uint64_t acc_a = 1, acc_c = 0, cur_a = kPcgMult, cur_c = inc;
+    while (delta) {
+        if (delta & 1u) {
+            acc_a *= cur_a;
+            acc_c = acc_c * cur_a + cur_c;
+        }
+        cur_c = (cur_a + 1u) * cur_c;
+        cur_a *= cur_a;
+        delta >>= 1u;
+    }
+    return {acc_a, acc_c};
+}
+
+// pcg32_srandom_r(initstate = seed, initseq = stream_id), then skip `offset`.
+struct StreamStart {
+    uint64_t state;  // state whose output is sample `offset`
+    uint64_t inc;
+};
+__host__ __device__ inline StreamStart pcg32_start(uint64_t seed, uint64_t stream_id, uint64_t offset) {
+    const uint64_t inc = (stream_id << 1u) | 1u;
+    uint64_t s = inc;  // 0 * M + inc
+    s += seed;
+    s = s * kPcgMult + inc;
+    const Affine j = lcg_jump(offset, inc);
+    return {j.a * s + j.c, inc};
+}
+
+// XSH-RR output of a state (the value produced *before* stepping).
+__device__ __forceinline__ uint32_t pcg32_output(uint64_t old) {
+    const uint32_t lo = static_cast<uint32_t>(old);
+    const uint32_t hi = static_cast<uint32_t>(old >> 32);
+    // bits 27..58 of (old ^ (old >> 18)) = funnel(lo,hi,27) ^ (hi >> 13)
+    const uint32_t xs = __funnelshift_r(lo, hi, 27) ^ (hi >> 13);
+    const uint32_t rot = hi >> 27;
+    return __funnelshift_r(xs, xs, rot);
+}
+
+// ------------------------------------------------------ uniform mappings --
+// f32 lattice uniform u = ((w >> 9) + 0.5) 2^-23, returned in reflected form:
+//   m  = all-ones iff u >= 1/2 (i.e. the reference predicate u < 0.5 is false)
+//   v  = min(u, 1-u) = (k' + 0.5) 2^-23 computed exactly as
+//        as_float(0x3F800000 | k') - (1 - 2^-24)   (Sterbenz; no I2F)
+struct Reflected {
+    float v;
+    uint32_t m;
+};
+__device__ __forceinline__ Reflected reflect_u32(uint32_t w) {
+    const uint32_t m = static_cast<uint32_t>(static_cast<int32_t>(w) >> 31);
+    const uint32_t kp = (w ^ m) >> 9;
+    const float v = __fsub_rn(__uint_as_float(0x3F800000u | kp), 0.99999994f);
+    return {v, m};
+}
+__device__ __forceinline__ float u32_to_f32(uint32_t w) {
+    return __fmul_rn(__uint2float_rn(w >> 9) + 0.5f, 0x1p-23f);
+}
+__device__ __forceinline__ double u32_to_f64(uint32_t w) {
+    return __dmul_rn(__dadd_rn(static_cast<double>(w), 0.5), 0x1p-32);
+}
+
+// ------------------------------------------------------ AS 241 (PPND16) --
+// exact_dist.py:30-62 coefficients (constant term first); evaluation order of
+// exact_dist.py:65-126.  Coefficients live in constant memory: every lane of
+// a warp reads the same word, so they are broadcast operands of DMUL/DADD.
+#define ARV_AS241_A 3.3871328727963666080e0, 1.3314166789178437745e2, 1.9715909503065514427e3, \
+    1.3731693765509461125e4, 4.5921953931549871457e4, 6.7265770927008700853e4,                 \
+    3.3430575583588128105e4, 2.5090809287301226727e3
+#define ARV_AS241_B 1.0, 4.2313330701600911252e1, 6.8718700749205790830e2,                  \
+    5.3941960214247511077e3, 2.1213794301586595867e4, 3.9307895800092710610e4,               \
+    2.8729085735721942674e4, 5.2264952788528545610e3
+#define ARV_AS241_C 1.42343711074968357734e0, 4.63033784615654529590e0, 5.76949722146069140550e0, \
+    3.64784832476320460504e0, 1.27045825245236838258e0, 2.41780725177450611770e-1,                 \
+    2.27238449892691845833e-2, 7.74545014278341407640e-4
+#define ARV_AS241_D 1.0, 2.05319162663775882187e0, 1.67638483018380384940e0,                   \
+    6.89767334985100004550e-1, 1.48103976427480074590e-1, 1.51986665636164571966e-2,          \
+    5.47593808499534494600e-4, 1.05075007164441684324e-9
+#define ARV_AS241_E 6.65790464350110377720e0, 5.46378491116411436990e0, 1.78482653991729133580e0, \
+    2.96560571828504891230e-1, 2.65321895265761230930e-2, 1.24266094738807843860e-3,               \
+    2.71155556874348757815e-5, 2.01033439929228813265e-7
+#define ARV_AS241_F 1.0, 5.99832206555887937690e-1, 1.36929880922735805310e-1,                 \
+    1.48753612908506148525e-2, 7.86869131145613259100e-4, 1.84631831751005468180e-5,          \
+    1.42151175831644588870e-7, 2.04426310338993978564e-15
+
+static __constant__ double kAS241d[6][8] = {{ARV_AS241_A}, {ARV_AS241_B}, {ARV_AS241_C},
+                                            {ARV_AS241_D}, {ARV_AS241_E}, {ARV_AS241_F}};
+// Same coefficients rounded to f32 (the single-precision evaluation).
+static __constant__ float kAS241f[6][8] = {{ARV_AS241_A}, {ARV_AS241_B}, {ARV_AS241_C},
+                                           {ARV_AS241_D}, {ARV_AS241_E}, {ARV_AS241_F}};
+
+// Horner with separately rounded multiply and add (numpy has no FMA).
+__device__ __forceinline__ double poly8d(int which, double x) {
+    double acc = kAS241d[which][7];
+#pragma unroll
+    for (int i = 6; i >= 0; --i) acc = __dadd_rn(__dmul_rn(acc, x), kAS241d[which][i]);
+    return acc;
+}
+__device__ __forceinline__ float poly8f(int which, float x) {
+    float acc = kAS241f[which][7];
+#pragma unroll
+    for (int i = 6; i >= 0; --i) acc = __fadd_rn(__fmul_rn(acc, x), kAS241f[which][i]);
+    return acc;
+}
+
+__device__ __forceinline__ double as241_f64(double u) {
+    const double q = __dsub_rn(u, 0.5);
+    if (fabs(q) <= 0.425) {
+        const double r = __dsub_rn(0.180625, __dmul_rn(q, q));
+        return __ddiv_rn(__dmul_rn(q, poly8d(0, r)), poly8d(1, r));
+    }
+    const bool upper = u > 0.5;
+    const double w = upper ? __dsub_rn(1.0, u) : u;
+    const double r = __dsqrt_rn(-log(w));
+    double val;
+    if (r <= 5.0) {
+        const double rn = __dsub_rn(r, 1.6);
+        val = __ddiv_rn(poly8d(2, rn), poly8d(3, rn));
+    } else {
+        const double rf = __dsub_rn(r, 5.0);
+        val = __ddiv_rn(poly8d(4, rf), poly8d(5, rf));
+    }
+    return upper ? val : -val;
+}
+
+__device__ __forceinline__ float as241_f32(float u) {
+    const float q = __fsub_rn(u, 0.5f);
+    if (fabsf(q) <= 0.425f) {
+        const float r = __fsub_rn(0.180625f, __fmul_rn(q, q));
+        return __fdiv_rn(__fmul_rn(q, poly8f(0, r)), poly8f(1, r));
+    }
+    const bool upper = u > 0.5f;
+    const float w = upper ? __fsub_rn(1.0f, u) : u;
+    const float r = __fsqrt_rn(-logf(w));
+    float val;
+    if (r <= 5.0f) {
+        const float rn = __fsub_rn(r, 1.6f);
+        val = __fdiv_rn(poly8f(2, rn), poly8f(3, rn));
+    } else {
+        const float rf = __fsub_rn(r, 5.0f);
+        val = __fdiv_rn(poly8f(4, rf), poly8f(5, rf));
+    }
+    return upper ? val : -val;
+}
+
+// ------------------------------------------------- dyadic index helpers --
+// _kernels.pyx:36 / :51 (exponent bits), with a memory-safety clamp at 0.
+__device__ __forceinline__ long long dyadic_idx64(double v, long long cap) {
+    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
+    const long long idx = 1022 - static_cast<long long>(bits >> 52);
+    return idx < cap ? idx : cap;
+}
+__device__ __forceinline__ long long dyadic_idx32(float v, long long cap) {
+    const unsigned int bits = __float_as_uint(v);
+    const long long idx = 126 - static_cast<long long>(bits >> 23);
+    return idx < cap ? idx : cap;
+}
+
+// Grid for a streaming kernel: enough CTAs to fill every SM `per_sm` times,
+// never more than the work needs.
+inline int stream_grid(int64_t work_items, int block, int per_sm) {
+    const int64_t need = (work_items + block - 1) / block;
+    const int64_t cap = static_cast<int64_t>(device_sm_count()) * per_sm;
+    int64_t g = need < cap ? need : cap;
+    return static_cast<int>(g < 1 ? 1 : g);
+}
+
+}  // namespace arv

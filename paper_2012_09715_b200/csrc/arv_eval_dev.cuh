@@ -1,0 +1,54 @@
+// Device evaluators shared by the drop-in kernels and the MLMC path kernels.
+#pragma once
+
+#include "arv_common.cuh"
+
+namespace arv {
+
+// _kernels.pyx:56-73 for one element; coefficient table `c` (DEG+1, K1).
+template <int DEG>
+__device__ __forceinline__ double dyadic_eval1(const double *c, int64_t K1, double ui) {
+    const bool pred = ui < 0.5;
+    const double v = pred ? ui : __dsub_rn(1.0, ui);
+    long long idx = dyadic_idx64(v, K1 - 1);
+    idx = idx < 0 ? 0 : idx;
+    double z = c[DEG * K1 + idx];
+#pragma unroll
+    for (int d = DEG - 1; d >= 0; --d) z = __dadd_rn(__dmul_rn(z, v), c[d * K1 + idx]);
+    return pred ? z : -z;
+}
+
+// _kernels.pyx:96-143 for one element.  stacks (2, n_knots, DEG+1, K1):
+// upper half at 0, lower at 1; knot bracketing j = min(floor(sqrt(nu /
+// (lam + nu)) (n_knots - 1)), n_knots - 2); linear interpolation in t.
+// All IEEE (div / sqrt round-to-nearest), separately rounded mul/add.
+template <int DEG>
+__device__ __forceinline__ double ncchi2_eval1(const double *tab, int64_t n_knots, int64_t K1, double nu, double ui,
+                                               double lam_i) {
+    const long long cap = K1 - 1;
+    const double shift = __dadd_rn(lam_i, nu);
+    const double scale2 = __dmul_rn(2.0, __dsqrt_rn(shift));
+    const double s = __dsqrt_rn(__ddiv_rn(nu, shift));
+    const double g = __dmul_rn(s, static_cast<double>(n_knots - 1));
+    long long j = static_cast<long long>(g);
+    j = j < n_knots - 2 ? j : n_knots - 2;
+    j = j < 0 ? 0 : j;
+    const double t = __dsub_rn(g, static_cast<double>(j));
+    const long long sel = ui < 0.5 ? 1 : 0;
+    const double v = sel ? ui : __dsub_rn(1.0, ui);
+    long long idx = dyadic_idx64(v, cap);
+    idx = idx < 0 ? 0 : idx;
+    const int64_t knot = (DEG + 1) * K1;
+    const double *t0 = tab + (sel * n_knots + j) * knot;
+    const double *t1 = t0 + knot;
+    double z0 = t0[DEG * K1 + idx];
+    double z1 = t1[DEG * K1 + idx];
+#pragma unroll
+    for (int d = DEG - 1; d >= 0; --d) {
+        z0 = __dadd_rn(__dmul_rn(z0, v), t0[d * K1 + idx]);
+        z1 = __dadd_rn(__dmul_rn(z1, v), t1[d * K1 + idx]);
+    }
+    return __dadd_rn(shift, __dmul_rn(scale2, __dadd_rn(z0, __dmul_rn(t, __dsub_rn(z1, z0)))));
+}
+
+}  // namespace arv

@@ -1,0 +1,471 @@
+// Nested MLMC level kernels: one thread per path, all path states in f64
+// registers, PCG32 stream state in registers, and in-CTA two-pass reduction
+// of the per-path differences into (count, mean, M2) partials that a second
+// one-CTA kernel merges in a fixed order (Chan), so statistics are bitwise
+// reproducible for a given (path_lo, path_count) whatever the scheduling.
+//
+// Reference loops restated (mlmc.py):
+//   GBM EM / Milstein        simulate_gbm_coupled   :164-229 (em_step :194-198)
+//   CIR truncated Euler      simulate_cir_coupled   :289-331
+//   CIR exact (chi^2)        simulate_cir_coupled   :253-287
+//   differences / estimator  difference, estimate_level_suite :341-411
+// Uniform for (fine step k, path p) = PCG32 output k * n_paths_total + p of
+// stream (seed, stream_id), mapped to (w + 0.5) 2^-32 -- the reference's
+// per-step `stream.uniforms(n_paths)` addressing (:200-202, :261-262).  A
+// thread reaches its first output with one jump and then advances by
+// n_paths_total per step with a single precomputed affine map, i.e. one
+// 64-bit multiply-add per step, as in a plain LCG.
+#include <cmath>
+
+#include "arv_common.cuh"
+#include "arv_eval_dev.cuh"
+#include "arv_ncchi2.cuh"
+
+namespace arv {
+
+constexpr int kLevelBlock = 256;
+constexpr int kFinalBlock = 256;
+
+struct LevelArgs {
+    double a, b, c;  // GBM: mu, sigma, -; CIR: kappa, theta, sigma
+    double x0, strike;
+    double dt_f, dt_c, sq_f;
+    int64_t n_f;
+    int level, payoff;
+    uint64_t s0, inc;   // stream state at output 0
+    Affine step;        // LCG^(n_paths_total)
+    int64_t path_lo, path_count;
+    // CIR exact
+    double nu_exact, nu_table, scale, decay_over_scale;
+};
+
+__device__ __forceinline__ double payoff_fn(double x, int payoff, double strike) {
+    return payoff == ARV_PAYOFF_CALL ? fmax(__dsub_rn(x, strike), 0.0) : x;
+}
+
+// mlmc.py:194-198 em_step: x (1 + mu dt + sg dw [+ 0.5 sg^2 (dw^2 - dt)])
+template <bool MIL>
+__device__ __forceinline__ double gbm_step(double x, double dw, double dt, double mu, double sg) {
+    double incr = __dadd_rn(__dmul_rn(mu, dt), __dmul_rn(sg, dw));
+    if (MIL) incr = __dadd_rn(incr, __dmul_rn(__dmul_rn(__dmul_rn(0.5, sg), sg), __dsub_rn(__dmul_rn(dw, dw), dt)));
+    return __dmul_rn(x, __dadd_rn(1.0, incr));
+}
+
+// mlmc.py:295-296 truncated Euler: x + kp (th - x) dt + sg sqrt|x| dw; the
+// Milstein variant (new, not in the reference) adds sg^2/4 (dw^2 - dt).
+template <bool MIL>
+__device__ __forceinline__ double cir_step(double x, double dw, double dt, double kp, double th, double sg) {
+    double r = __dadd_rn(x, __dmul_rn(__dmul_rn(kp, __dsub_rn(th, x)), dt));
+    r = __dadd_rn(r, __dmul_rn(__dmul_rn(sg, __dsqrt_rn(fabs(x))), dw));
+    if (MIL) r = __dadd_rn(r, __dmul_rn(__dmul_rn(__dmul_rn(0.25, sg), sg), __dsub_rn(__dmul_rn(dw, dw), dt)));
+    return r;
+}
+
+// ------------------------------------------------------ CTA reduction --
+// Two-pass (count, mean, M2) of NK values per thread over the CTA.
+template <int NK>
+__device__ __forceinline__ void cta_moments(const double (&d)[NK], bool valid, double *partial_out) {
+    __shared__ double red[NK][kLevelBlock / 32];
+    __shared__ double mean_sh[NK];
+    __shared__ int cnt_sh;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cnt_w = __popc(__ballot_sync(0xffffffffu, valid));
+    if (threadIdx.x == 0) cnt_sh = 0;
+    __syncthreads();
+    if (lane == 0) atomicAdd(&cnt_sh, cnt_w);
+    double s[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+        s[k] = valid ? d[k] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
+        if (lane == 0) red[k][warp] = s[k];
+    }
+    __syncthreads();
+    const int count = cnt_sh;
+    if (threadIdx.x < NK) {
+        double t = 0.0;
+        for (int w = 0; w < kLevelBlock / 32; ++w) t += red[threadIdx.x][w];
+        mean_sh[threadIdx.x] = count > 0 ? t / count : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+        const double dv = valid ? d[k] - mean_sh[k] : 0.0;
+        s[k] = dv * dv;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
+    }
+    __syncthreads();  // everyone has read mean_sh / red
+#pragma unroll
+    for (int k = 0; k < NK; ++k)
+        if (lane == 0) red[k][warp] = s[k];
+    __syncthreads();
+    if (threadIdx.x < NK) {
+        double t = 0.0;
+        for (int w = 0; w < kLevelBlock / 32; ++w) t += red[threadIdx.x][w];
+        double *o = partial_out + 3 * threadIdx.x;
+        o[0] = count;
+        o[1] = mean_sh[threadIdx.x];
+        o[2] = t;
+    }
+}
+
+__device__ __forceinline__ void chan_merge(double &n, double &mean, double &m2, double nb, double mb, double m2b) {
+    if (nb == 0.0) return;
+    if (n == 0.0) {
+        n = nb;
+        mean = mb;
+        m2 = m2b;
+        return;
+    }
+    const double tot = n + nb;
+    const double delta = mb - mean;
+    mean += delta * (nb / tot);
+    m2 += m2b + delta * delta * (n * nb / tot);
+    n = tot;
+}
+
+// Merge n_parts partials (n_parts x NK x 3) into out (NK x 3), fixed order.
+__global__ void __launch_bounds__(kFinalBlock) k_finalize(const double *__restrict__ parts, int64_t n_parts, int nk,
+                                                          double *__restrict__ out) {
+    __shared__ double sh[kFinalBlock][3];
+    for (int k = 0; k < nk; ++k) {
+        const int64_t per = (n_parts + kFinalBlock - 1) / kFinalBlock;
+        const int64_t lo = threadIdx.x * per;
+        const int64_t hi = lo + per < n_parts ? lo + per : n_parts;
+        double n = 0.0, mean = 0.0, m2 = 0.0;
+        for (int64_t i = lo; i < hi; ++i) {
+            const double *p = parts + (i * nk + k) * 3;
+            chan_merge(n, mean, m2, p[0], p[1], p[2]);
+        }
+        sh[threadIdx.x][0] = n;
+        sh[threadIdx.x][1] = mean;
+        sh[threadIdx.x][2] = m2;
+        __syncthreads();
+        for (int stride = 1; stride < kFinalBlock; stride <<= 1) {
+            if ((threadIdx.x % (2 * stride)) == 0 && threadIdx.x + stride < kFinalBlock) {
+                double a0 = sh[threadIdx.x][0], a1 = sh[threadIdx.x][1], a2 = sh[threadIdx.x][2];
+                chan_merge(a0, a1, a2, sh[threadIdx.x + stride][0], sh[threadIdx.x + stride][1],
+                           sh[threadIdx.x + stride][2]);
+                sh[threadIdx.x][0] = a0;
+                sh[threadIdx.x][1] = a1;
+                sh[threadIdx.x][2] = a2;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            out[3 * k + 0] = sh[0][0];
+            out[3 * k + 1] = sh[0][1];
+            out[3 * k + 2] = sh[0][2];
+        }
+        __syncthreads();
+    }
+}
+
+// --------------------------------------------------- Gaussian schemes --
+// SCHEME: ARV_SCHEME_EM, _MILSTEIN (GBM), _CIR_EULER_TRUNCATED, _CIR_MILSTEIN_TRUNCATED
+template <int DEG, int SCHEME>
+__global__ void __launch_bounds__(kLevelBlock) k_gaussian_level(LevelArgs A, const double *__restrict__ coeffs,
+                                                                int64_t K1, double *__restrict__ parts,
+                                                                double *__restrict__ paths) {
+    extern __shared__ double smd[];
+    for (int i = threadIdx.x; i < (DEG + 1) * K1; i += blockDim.x) smd[i] = __ldg(coeffs + i);
+    __syncthreads();
+    constexpr bool GBM = SCHEME == ARV_SCHEME_EM || SCHEME == ARV_SCHEME_MILSTEIN;
+    constexpr bool MIL = SCHEME == ARV_SCHEME_MILSTEIN || SCHEME == ARV_SCHEME_CIR_MILSTEIN_TRUNCATED;
+
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool valid = i < A.path_count;
+    double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (valid) {
+        const uint64_t p = static_cast<uint64_t>(A.path_lo + i);
+        const Affine jp = lcg_jump(p, A.inc);
+        uint64_t s = jp.a * A.s0 + jp.c;
+        const double x0 = A.x0, dt_f = A.dt_f, dt_c = A.dt_c, sq_f = A.sq_f;
+        double xf_e = x0, xc_e = x0, xf_a = x0, xc_a = x0;
+        auto step = [&](double x, double dw, double dt) -> double {
+            if constexpr (GBM) return gbm_step<MIL>(x, dw, dt, A.a, A.b);
+            else return cir_step<MIL>(x, dw, dt, A.a, A.b, A.c);
+        };
+        for (int64_t pair = 0; pair < A.n_f / 2; ++pair) {
+            const double u1 = u32_to_f64(pcg32_output(s));
+            s = A.step.a * s + A.step.c;
+            const double u2 = u32_to_f64(pcg32_output(s));
+            s = A.step.a * s + A.step.c;
+            const double z1 = as241_f64(u1), z2 = as241_f64(u2);
+            xf_e = step(step(xf_e, __dmul_rn(sq_f, z1), dt_f), __dmul_rn(sq_f, z2), dt_f);
+            xc_e = step(xc_e, __dmul_rn(sq_f, __dadd_rn(z1, z2)), dt_c);
+            const double w1 = dyadic_eval1<DEG>(smd, K1, u1), w2 = dyadic_eval1<DEG>(smd, K1, u2);
+            xf_a = step(step(xf_a, __dmul_rn(sq_f, w1), dt_f), __dmul_rn(sq_f, w2), dt_f);
+            xc_a = step(xc_a, __dmul_rn(sq_f, __dadd_rn(w1, w2)), dt_c);
+        }
+        if (A.n_f & 1) {
+            const double u1 = u32_to_f64(pcg32_output(s));
+            xf_e = step(xf_e, __dmul_rn(sq_f, as241_f64(u1)), dt_f);
+            xf_a = step(xf_a, __dmul_rn(sq_f, dyadic_eval1<DEG>(smd, K1, u1)), dt_f);
+        }
+        const double fe = payoff_fn(xf_e, A.payoff, A.strike);
+        const double fa = payoff_fn(xf_a, A.payoff, A.strike);
+        const double ce = A.level > 0 ? payoff_fn(xc_e, A.payoff, A.strike) : 0.0;
+        const double ca = A.level > 0 ? payoff_fn(xc_a, A.payoff, A.strike) : 0.0;
+        // mlmc.py:341-353 (two_way exact / approx, four_way) and plain
+        d[0] = __dsub_rn(fe, ce);
+        d[1] = __dsub_rn(fa, ca);
+        d[2] = __dadd_rn(__dsub_rn(__dsub_rn(fe, ce), fa), ca);
+        d[3] = fe;
+        d[4] = fa;
+        if (paths) {
+            paths[i] = fe;
+            paths[A.path_count + i] = ce;
+            paths[2 * A.path_count + i] = fa;
+            paths[3 * A.path_count + i] = ca;
+        }
+    }
+    cta_moments<ARV_NKIND>(d, valid, parts + static_cast<int64_t>(blockIdx.x) * 3 * ARV_NKIND);
+}
+
+// ----------------------------------------------------------- CIR exact --
+template <int DEG>
+__global__ void __launch_bounds__(kLevelBlock) k_cir_exact_level(LevelArgs A, const double *__restrict__ stacks,
+                                                                 int64_t n_knots, int64_t K1, int use_smem,
+                                                                 double *__restrict__ parts,
+                                                                 double *__restrict__ paths,
+                                                                 unsigned long long *__restrict__ n_fail) {
+    extern __shared__ double smd[];
+    const double *tab = stacks;
+    if (use_smem) {
+        const int64_t total = 2 * n_knots * (DEG + 1) * K1;
+        for (int64_t k = threadIdx.x; k < total; k += blockDim.x) smd[k] = __ldg(stacks + k);
+        __syncthreads();
+        tab = smd;
+    }
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool valid = i < A.path_count;
+    double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (valid) {
+        const uint64_t p = static_cast<uint64_t>(A.path_lo + i);
+        const Affine jp = lcg_jump(p, A.inc);
+        uint64_t s = jp.a * A.s0 + jp.c;
+        double x_e = A.x0, x_a = A.x0;
+        unsigned fails = 0;
+        for (int64_t k = 0; k < A.n_f; ++k) {
+            const double u = u32_to_f64(pcg32_output(s));
+            s = A.step.a * s + A.step.c;
+            // mlmc.py:264-268 approximate side (state clamped before lambda)
+            const double lam_a = __dmul_rn(fmax(x_a, 0.0), A.decay_over_scale);
+            x_a = __dmul_rn(A.scale, ncchi2_eval1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_a));
+            // mlmc.py:269-278 exact side, warm-started from the table
+            const double lam_e = __dmul_rn(x_e, A.decay_over_scale);
+            const double warm = ncchi2_eval1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_e);
+            const NcQuantile q = ncchi2_quantile(u, A.nu_exact, lam_e, warm);
+            fails += q.resid > 1e-8;
+            x_e = __dmul_rn(A.scale, q.x);
+        }
+        if (fails && n_fail) atomicAdd(n_fail, static_cast<unsigned long long>(fails));
+        const double fe = payoff_fn(x_e, A.payoff, A.strike);
+        const double fa = payoff_fn(x_a, A.payoff, A.strike);
+        // coarse slots repeat the fine payoffs (mlmc.py:281-286), so both
+        // two-way differences vanish; slot 2 carries the exact - approx
+        // correction of reproduce.py:299-301, slots 3/4 the process values.
+        d[2] = __dsub_rn(fe, fa);
+        d[3] = fe;
+        d[4] = fa;
+        if (paths) {
+            paths[i] = fe;
+            paths[A.path_count + i] = fe;  // coarse slots repeat fine (mlmc.py:281-286)
+            paths[2 * A.path_count + i] = fa;
+            paths[3 * A.path_count + i] = fa;
+        }
+    }
+    cta_moments<ARV_NKIND>(d, valid, parts + static_cast<int64_t>(blockIdx.x) * 3 * ARV_NKIND);
+}
+
+// -------------------------------------------------- standalone ncchi2 --
+__global__ void __launch_bounds__(256) k_ncchi2_inv(const double *__restrict__ u, const double *__restrict__ lam,
+                                                    int64_t nlam, double nu, const double *__restrict__ x0,
+                                                    double *__restrict__ out, double *__restrict__ resid, int64_t n) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double li = nlam == 1 ? lam[0] : lam[i];
+        const NcQuantile q = ncchi2_quantile(u[i], nu, li, x0 ? x0[i] : -1.0);
+        out[i] = q.x;
+        if (resid) resid[i] = q.resid;
+    }
+}
+__global__ void __launch_bounds__(256) k_ncchi2_cdf(const double *__restrict__ x, const double *__restrict__ lam,
+                                                    int64_t nlam, double nu, double *__restrict__ out, int64_t n) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double li = nlam == 1 ? lam[0] : lam[i];
+        const double xi = x[i];
+        out[i] = xi <= 0.0 ? 0.0 : ncchi2_cdf_minus(xi, nu, li, 0.0, 1.0).resid;
+    }
+}
+
+// ---------------------------------------------------------------- host --
+static int fill_common(const arv_level_spec *sp, LevelArgs &A) {
+    if (!sp) return set_error(ARV_ERR_CONFIG, "null level spec");
+    if (sp->level < 0) return set_error(ARV_ERR_CONFIG, "level must be >= 0");
+    if (sp->n0 < 1) return set_error(ARV_ERR_CONFIG, "n0 must be >= 1");
+    if (sp->payoff != ARV_PAYOFF_IDENTITY && sp->payoff != ARV_PAYOFF_CALL)
+        return set_error(ARV_ERR_CONFIG, "unknown payoff %d", sp->payoff);
+    if (sp->path_count < 0 || sp->path_lo < 0 || sp->path_lo + sp->path_count > sp->n_paths_total)
+        return set_error(ARV_ERR_CONFIG, "path range [%lld, +%lld) outside n_paths_total=%lld", (long long)sp->path_lo,
+                         (long long)sp->path_count, (long long)sp->n_paths_total);
+    if (sp->level > 40) return set_error(ARV_ERR_CONFIG, "level too large");
+    A.a = sp->a;
+    A.b = sp->b;
+    A.c = sp->c;
+    A.x0 = sp->x0;
+    A.strike = sp->strike;
+    A.level = sp->level;
+    A.payoff = sp->payoff;
+    A.n_f = static_cast<int64_t>(sp->n0) << sp->level;
+    A.dt_f = sp->t_end / static_cast<double>(A.n_f);  // mlmc.py:119-120
+    A.dt_c = 2.0 * A.dt_f;
+    A.sq_f = std::sqrt(A.dt_f);
+    const StreamStart st = pcg32_start(sp->seed, sp->stream_id, 0);
+    A.s0 = st.state;
+    A.inc = st.inc;
+    A.step = lcg_jump(static_cast<uint64_t>(sp->n_paths_total), st.inc);
+    A.path_lo = sp->path_lo;
+    A.path_count = sp->path_count;
+    A.nu_exact = A.nu_table = A.scale = A.decay_over_scale = 0.0;
+    return ARV_OK;
+}
+
+static int64_t n_blocks_for(int64_t count) { return (count + kLevelBlock - 1) / kLevelBlock; }
+
+static int run_finalize(double *parts, int64_t nb, double *stats, cudaStream_t s, const char *what) {
+    k_finalize<<<1, kFinalBlock, 0, s>>>(parts, nb, ARV_NKIND, stats);
+    note_launch();
+    return check_launch(what);
+}
+
+}  // namespace arv
+
+using namespace arv;
+
+extern "C" {
+
+int64_t arv_mlmc_workspace_bytes(int64_t path_count) {
+    const int64_t nb = n_blocks_for(path_count < 1 ? 1 : path_count);
+    return nb * 3 * ARV_NKIND * static_cast<int64_t>(sizeof(double));
+}
+
+int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, int degree, int64_t K1, double *stats,
+                            double *paths, void *workspace, int64_t workspace_bytes, void *stream) {
+    LevelArgs A;
+    if (int rc = fill_common(spec, A)) return rc;
+    const int scheme = spec->scheme;
+    if (scheme == ARV_SCHEME_EM || scheme == ARV_SCHEME_MILSTEIN) {
+        if (!(spec->b > 0 && spec->x0 > 0 && spec->t_end > 0))
+            return set_error(ARV_ERR_CONFIG, "GBM requires sigma > 0, x0 > 0, t_end > 0");
+    } else if (scheme == ARV_SCHEME_CIR_EULER_TRUNCATED || scheme == ARV_SCHEME_CIR_MILSTEIN_TRUNCATED) {
+        if (!(spec->a > 0 && spec->b > 0 && spec->c > 0 && spec->x0 > 0 && spec->t_end > 0))
+            return set_error(ARV_ERR_CONFIG, "CIR requires kappa, theta, sigma, x0, t_end > 0");
+    } else {
+        return set_error(ARV_ERR_CONFIG, "arv_mlmc_gaussian_level cannot run scheme %d", scheme);
+    }
+    if (K1 < 2 || K1 > 4096) return set_error(ARV_ERR_CONFIG, "bad table interval count");
+    if (spec->path_count < 1) return set_error(ARV_ERR_CONFIG, "need at least one path");
+    const int64_t nb = n_blocks_for(spec->path_count);
+    if (workspace_bytes < nb * 3 * ARV_NKIND * static_cast<int64_t>(sizeof(double)))
+        return set_error(ARV_ERR_CONFIG, "workspace too small");
+    double *parts = static_cast<double *>(workspace);
+    const size_t smem = sizeof(double) * (degree + 1) * K1;
+    cudaStream_t s = as_stream(stream);
+#define ARV_LAUNCH(D, S) k_gaussian_level<D, S><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths)
+#define ARV_SCHEMES(D)                                                                      \
+    case D:                                                                                 \
+        switch (scheme) {                                                                   \
+            case ARV_SCHEME_EM: ARV_LAUNCH(D, ARV_SCHEME_EM); break;                        \
+            case ARV_SCHEME_MILSTEIN: ARV_LAUNCH(D, ARV_SCHEME_MILSTEIN); break;            \
+            case ARV_SCHEME_CIR_EULER_TRUNCATED: ARV_LAUNCH(D, ARV_SCHEME_CIR_EULER_TRUNCATED); break; \
+            default: ARV_LAUNCH(D, ARV_SCHEME_CIR_MILSTEIN_TRUNCATED); break;               \
+        }                                                                                   \
+        break;
+    switch (degree) {
+        ARV_SCHEMES(1)
+        ARV_SCHEMES(2)
+        ARV_SCHEMES(3)
+        ARV_SCHEMES(4)
+        ARV_SCHEMES(5)
+        default: return set_error(ARV_ERR_CONFIG, "polynomial degree must be in [1, 5], got %d", degree);
+    }
+#undef ARV_SCHEMES
+#undef ARV_LAUNCH
+    note_launch();
+    if (int rc = check_launch("arv_mlmc_gaussian_level")) return rc;
+    return run_finalize(parts, nb, stats, s, "arv_mlmc_gaussian_level(finalize)");
+}
+
+int arv_mlmc_cir_exact_level(const arv_level_spec *spec, const double *stacks, int64_t n_knots, int degree, int64_t K1,
+                             double nu, double *stats, double *paths, int64_t *n_fail, void *workspace,
+                             int64_t workspace_bytes, void *stream) {
+    LevelArgs A;
+    if (int rc = fill_common(spec, A)) return rc;
+    if (spec->scheme != ARV_SCHEME_CIR_EXACT) return set_error(ARV_ERR_CONFIG, "cir_exact level needs scheme CIR_EXACT");
+    const double kappa = spec->a, theta = spec->b, sigma = spec->c;
+    if (!(kappa > 0 && theta > 0 && sigma > 0 && spec->x0 > 0 && spec->t_end > 0))
+        return set_error(ARV_ERR_CONFIG, "CIR requires kappa, theta, sigma, x0, t_end > 0");
+    if (!(nu > 0)) return set_error(ARV_ERR_CONFIG, "nu must be > 0");
+    if (n_knots < 2 || K1 < 2) return set_error(ARV_ERR_CONFIG, "bad ncchi2 table shape");
+    if (spec->path_count < 1) return set_error(ARV_ERR_CONFIG, "need at least one path");
+    // exact_dist.py:561-564 (cir_transition_params) and mlmc.py:254-257
+    const double dt = A.dt_f;
+    const double decay = std::exp(-kappa * dt);
+    A.scale = sigma * sigma * (1.0 - decay) / (4.0 * kappa);
+    A.nu_exact = 4.0 * kappa * theta / (sigma * sigma);
+    A.decay_over_scale = std::exp(-kappa * dt) / A.scale;
+    A.nu_table = nu;
+    const int64_t nb = n_blocks_for(spec->path_count);
+    if (workspace_bytes < nb * 3 * ARV_NKIND * static_cast<int64_t>(sizeof(double)))
+        return set_error(ARV_ERR_CONFIG, "workspace too small");
+    double *parts = static_cast<double *>(workspace);
+    const size_t bytes = sizeof(double) * 2 * n_knots * (degree + 1) * K1;
+    const int use_smem = bytes <= 160 * 1024;
+    const size_t smem = use_smem ? bytes : 0;
+    cudaStream_t s = as_stream(stream);
+    unsigned long long *nf = reinterpret_cast<unsigned long long *>(n_fail);
+#define ARV_CASE(D)                                                                                          \
+    case D:                                                                                                  \
+        if (smem > 48 * 1024)                                                                                \
+            cudaFuncSetAttribute(k_cir_exact_level<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        k_cir_exact_level<D><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, stacks, n_knots, K1, use_smem, parts, paths, nf); \
+        break;
+    switch (degree) {
+        ARV_CASE(1)
+        ARV_CASE(2)
+        ARV_CASE(3)
+        ARV_CASE(4)
+        ARV_CASE(5)
+        default: return set_error(ARV_ERR_CONFIG, "polynomial degree must be in [1, 5], got %d", degree);
+    }
+#undef ARV_CASE
+    note_launch();
+    if (int rc = check_launch("arv_mlmc_cir_exact_level")) return rc;
+    return run_finalize(parts, nb, stats, s, "arv_mlmc_cir_exact_level(finalize)");
+}
+
+int arv_ncchi2_inv_cdf(const double *u, const double *lam, int64_t nlam, double nu, const double *x0, double *out,
+                       double *resid, int64_t n, void *stream) {
+    if (!(nu > 0)) return set_error(ARV_ERR_DOMAIN, "degrees of freedom must be > 0");
+    if (nlam != 1 && nlam != n) return set_error(ARV_ERR_CONFIG, "per-element lambda must match the shape of u");
+    if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
+    k_ncchi2_inv<<<stream_grid(n, 256, 8), 256, 0, as_stream(stream)>>>(u, lam, nlam, nu, x0, out, resid, n);
+    note_launch();
+    return check_launch("arv_ncchi2_inv_cdf");
+}
+
+int arv_ncchi2_cdf(const double *x, const double *lam, int64_t nlam, double nu, double *out, int64_t n, void *stream) {
+    if (!(nu > 0)) return set_error(ARV_ERR_DOMAIN, "degrees of freedom must be > 0");
+    if (nlam != 1 && nlam != n) return set_error(ARV_ERR_CONFIG, "per-element lambda must match the shape of x");
+    if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
+    k_ncchi2_cdf<<<stream_grid(n, 256, 8), 256, 0, as_stream(stream)>>>(x, lam, nlam, nu, out, n);
+    note_launch();
+    return check_launch("arv_ncchi2_cdf");
+}
+
+}  // extern "C"

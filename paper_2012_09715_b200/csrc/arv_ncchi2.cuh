@@ -1,0 +1,160 @@
+// Device non-central chi-squared CDF / density / quantile (f64).
+//
+// Replaces, for the CIR exact transition, the reference's
+// ncchi2_inv_cdf_batch per-element-lambda path (exact_dist.py:381-461):
+// bisection-safeguarded Newton (_vector_newton, exact_dist.py:348-378) in the
+// bracket [0, lam + nu + 20 sqrt(2(lam+nu)) + 100] with the tolerance
+// tol_f = min(1e-9, max(1e-13, 1e-4 min(u, 1-u))) and the residual contract
+// |F(x) - u| <= 1e-8 (exact_dist.py:452-460).  The reference evaluates F with
+// scipy's CDFLIB chndtr; here F is the Poisson mixture of regularized lower
+// incomplete gammas (the series of exact_dist.py:215-235),
+//     F(x; nu, lam) = sum_j Pois(j; lam/2) P(nu/2 + j, x/2),
+// evaluated from the Poisson mode outwards with the two-term recurrences
+//     P(a+1, y) = P(a, y) - G(a),  G(a) = y^a e^-y / Gamma(a+1),
+//     G(a+1) = G(a) y / (a+1),     Pois(j+1) = Pois(j) h / (j+1),
+// (the Benton-Krishnamoorthy organisation of Ding's series), so one pass
+// yields F and the density f(x) = 1/2 sum_j Pois(j) G(nu/2 + j - 1).  The
+// mode term P(a, y) comes from the power series (y < a+1) or the Lentz
+// continued fraction of Q (y >= a+1); whichever side is smaller is carried
+// through the recurrence, so tails keep their relative accuracy.  Poisson
+// weights are renormalised by their computed sum, cancelling the common
+// rounding of exp/lgamma in the mode weight.
+#pragma once
+
+#include "arv_common.cuh"
+
+namespace arv {
+
+struct GammaPQ {
+    double small;  // P if lower, else Q
+    bool lower;
+    double G;      // y^a e^-y / Gamma(a+1)
+};
+
+// Regularized incomplete gamma at (a, y), a > 0, y > 0.
+__device__ inline GammaPQ gamma_pq(double a, double y) {
+    const double lg = lgamma(a + 1.0);
+    const double G = exp(a * log(y) - y - lg);
+    GammaPQ r;
+    r.G = G;
+    if (y < a + 1.0) {
+        // P = G * sum_{n>=0} y^n / ((a+1)...(a+n))
+        double sum = 1.0, term = 1.0;
+        for (int n = 1; n < 2000; ++n) {
+            term *= y / (a + n);
+            sum += term;
+            if (term < sum * 1e-17) break;
+        }
+        r.small = G * sum;
+        r.lower = true;
+    } else {
+        // Q = (G a / y) * y / (y + 1 - a - 1(1-a)/(y + 3 - a - ...)) (modified Lentz)
+        const double tiny = 1e-300;
+        double b = y + 1.0 - a;
+        double c = 1.0 / tiny;
+        double d = 1.0 / b;
+        double h = d;
+        for (int i = 1; i < 2000; ++i) {
+            const double an = -i * (i - a);
+            b += 2.0;
+            d = an * d + b;
+            if (fabs(d) < tiny) d = tiny;
+            c = b + an / c;
+            if (fabs(c) < tiny) c = tiny;
+            d = 1.0 / d;
+            const double del = d * c;
+            h *= del;
+            if (fabs(del - 1.0) < 1e-16) break;
+        }
+        r.small = G * a * h;  // e^-y y^a / Gamma(a) * h
+        r.lower = false;
+    }
+    return r;
+}
+
+struct NcCdf {
+    double resid;  // F(x) - u, computed on the accurate side
+    double pdf;
+};
+
+// F(x) - u and f(x) for x > 0.  `one_minus_u` is exact for u >= 1/2.
+__device__ inline NcCdf ncchi2_cdf_minus(double x, double nu, double lam, double u, double one_minus_u) {
+    const double y = 0.5 * x;
+    const double a0 = 0.5 * nu;
+    const double h = 0.5 * lam;
+    const double kd = floor(h);
+    const long long k = static_cast<long long>(kd);
+    const double pk = h > 0.0 ? exp(-h + kd * log(h) - lgamma(kd + 1.0)) : 1.0;
+
+    const GammaPQ g = gamma_pq(a0 + kd, y);
+    const bool lower = g.lower;
+    // Mode term.  Carried side S_j: P_j (lower) or Q_j (upper).
+    double wsum = pk;
+    double acc = pk * g.small;
+    // density: 1/2 pk G(a0 + k - 1) = 1/2 pk G_k (a0 + k) / y
+    double dens = pk * g.G * (a0 + kd) / y;
+
+    // forward j = k+1, k+2, ...
+    {
+        double p = pk, S = g.small, G = g.G;
+        for (long long j = k + 1; j < k + 100000; ++j) {
+            const double jd = static_cast<double>(j);
+            p *= h / jd;
+            // S_j from S_{j-1}: P decreases by G_{j-1}, Q increases by it
+            S = lower ? fmax(S - G, 0.0) : S + G;
+            dens += p * G;  // G_{j-1} = G(a0 + j - 1)
+            G *= y / (a0 + jd);
+            wsum += p;
+            acc += p * S;
+            if (p < 1e-18 && jd > h) break;
+        }
+    }
+    // backward j = k-1, ..., 0
+    {
+        double p = pk, S = g.small, G = g.G;
+        for (long long j = k - 1; j >= 0; --j) {
+            const double jd = static_cast<double>(j);
+            p *= (jd + 1.0) / h;
+            G *= (a0 + jd + 1.0) / y;  // G_j = G_{j+1} (a0 + j + 1) / y
+            S = lower ? S + G : fmax(S - G, 0.0);
+            wsum += p;
+            acc += p * S;
+            dens += p * G * (a0 + jd) / y;  // G_{j-1}
+            if (p < 1e-18) break;
+        }
+    }
+    NcCdf r;
+    const double side = acc / wsum;
+    r.resid = lower ? side - u : one_minus_u - side;
+    r.pdf = 0.5 * dens / wsum;
+    return r;
+}
+
+struct NcQuantile {
+    double x;
+    double resid;  // |F(x) - u|
+};
+
+// exact_dist.py:381-461 contract, per element, warm start x0 (<= 0: mean).
+__device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, double x0) {
+    const double one_minus_u = 1.0 - u;
+    double hi = lam + nu + 20.0 * sqrt(2.0 * (lam + nu)) + 100.0;
+    double lo = 0.0;
+    const double tol_f = fmin(1e-9, fmax(1e-13, 1e-4 * fmin(u, one_minus_u)));
+    double x = x0 > 0.0 ? x0 : lam + nu;
+    x = fmin(fmax(x, 1e-8), hi);
+    NcCdf c = ncchi2_cdf_minus(x, nu, lam, u, one_minus_u);
+    for (int it = 0; it < 80; ++it) {
+        if (fabs(c.resid) <= tol_f) break;
+        if (c.resid > 0.0) hi = x;
+        else lo = x;
+        double xn = x - c.resid / c.pdf;
+        if (!isfinite(xn) || xn <= lo || xn >= hi) xn = 0.5 * (lo + hi);
+        x = xn;
+        c = ncchi2_cdf_minus(x, nu, lam, u, one_minus_u);
+        if (hi - lo < 1e-15 * hi) break;
+    }
+    return {x, fabs(c.resid)};
+}
+
+}  // namespace arv

@@ -1,0 +1,348 @@
+"""Hot-path evaluation: uniforms in, approximate random variables out.
+
+Mirrors the reference sampler API (approxrv/sampler.py:91-223): the eval
+wrappers keep their names, argument meaning and errors, and route through
+the drop-in kernel plugin (``_kernels``) on the device.  Inputs may be host
+scalars/arrays (results come back to the host, like the reference) or CUDA
+tensors (results stay on the device).
+
+The uniform source is :class:`Pcg32Stream` (BASELINE.json: PCG32, seed 42,
+stream 0), a counter-addressable stream like the reference's
+``UniformStream`` (sampler.py:26-66): output ``i`` of ``(seed, stream_id)``
+is fixed, ``counter`` advances by the words drawn, and any range can be
+produced independently -- which is how samples shard across GPUs.  Its
+``sample`` method is the fused generator: PCG32 -> table -> 128-bit stores,
+with no input traffic at all.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as dev
+from . import _kernels as kernels
+from ._native import call
+from .errors import ConfigError, DomainError
+from .tables import ConstantTable, DyadicPolyTable, NcChi2Table, SubDyadicTable
+
+_MAX64 = (1 << 64) - 1
+
+
+# ---------------------------------------------------------------------------
+# Reference eval wrappers (sampler.py:91-206)
+# ---------------------------------------------------------------------------
+
+def _as_batch(u, dtype=torch.float64):
+    """(device tensor, scalar?, host?) -- sampler.py:91-94 on the device."""
+    if dev.is_device_tensor(u):
+        return dev.to_device(u.reshape(-1) if u.dim() else u.reshape(1), dtype, u.device), u.dim() == 0, False
+    arr = np.asarray(u, dtype=np.float64)
+    scalar = arr.ndim == 0
+    return dev.to_device(np.atleast_1d(arr).reshape(-1), dtype), scalar, True
+
+
+def _result(t: torch.Tensor, scalar: bool, host: bool, out=None):
+    if out is not None:
+        dev.copy_out(out, t)
+        return float(t[0]) if scalar else out
+    if scalar:
+        return float(t[0])
+    return t.cpu().numpy() if host else t
+
+
+def _coeffs(table, attr):
+    return getattr(table, attr)
+
+
+def eval_constant(table, u, out=None):
+    """values[floor(2^q u)] per element (sampler.py:97-108)."""
+    ud, scalar, host = _as_batch(u)
+    od = torch.empty_like(ud)
+    kernels.constant_eval(table.values, ud, od)
+    return _result(od, scalar, host, out)
+
+
+def dyadic_index(u, n_intervals: int = 1 << 62, dtype=np.float64):
+    """Capped dyadic interval index from the float's exponent bits (sampler.py:111-124)."""
+    if dtype == np.float32:
+        ud, scalar, host = _as_batch(u, torch.float32)
+        idx = kernels.dyadic_index32(ud, n_intervals)
+    else:
+        ud, scalar, host = _as_batch(u)
+        idx = kernels.dyadic_index(ud, n_intervals)
+    if scalar:
+        return int(idx[0])
+    return idx.cpu().numpy() if host else idx
+
+
+def _eval_general_decay(table, ud: torch.Tensor) -> torch.Tensor:
+    """Analysis path for decay != 1/2 (sampler.py:127-141), as device tensor ops."""
+    pred = ud < 0.5
+    v = torch.where(pred, ud, 1.0 - ud)
+    t = torch.log(2.0 * v) / math.log(table.decay)
+    idx = torch.clamp(torch.ceil(t).to(torch.int64), 0, table.n_intervals)
+    c = dev.table_on_device(table.coeffs, torch.float64, ud.device)
+    acc = c[-1][idx]
+    for row in range(c.shape[0] - 2, -1, -1):
+        acc = acc * v + c[row][idx]
+    return torch.where(pred, acc, -acc)
+
+
+def eval_dyadic(table, u, dtype=np.float64, out=None):
+    """Reflect-about-1/2, exponent-indexed Horner evaluation (sampler.py:144-172)."""
+    if isinstance(table, SubDyadicTable):
+        return eval_subdyadic(table, u, out=out)
+    if getattr(table, "decay", 0.5) != 0.5:
+        if dtype == np.float32:
+            raise ConfigError("the float32 fast path requires decay rate 1/2")
+        ud, scalar, host = _as_batch(u)
+        return _result(_eval_general_decay(table, ud), scalar, host, out)
+    if dtype == np.float32:
+        ud, scalar, host = _as_batch(u, torch.float32)
+        od = torch.empty_like(ud)
+        kernels.dyadic_eval32(table.coeffs32, ud, od)
+    else:
+        ud, scalar, host = _as_batch(u)
+        od = torch.empty_like(ud)
+        kernels.dyadic_eval(table.coeffs, ud, od)
+    return _result(od, scalar, host, out)
+
+
+def eval_subdyadic(table: SubDyadicTable, u, out=None):
+    """Octave x sub-interval table, float32 arithmetic (BASELINE.json config 2)."""
+    ud, scalar, host = _as_batch(u, torch.float32)
+    od = torch.empty_like(ud)
+    kernels.subdyadic_eval32(table.coeffs32, table.sub_bits, ud, od)
+    return _result(od, scalar, host, out)
+
+
+def eval_ncchi2(table, u, lam, out=None):
+    """Approximate non-central chi-squared quantiles (sampler.py:175-193)."""
+    ud, scalar, host = _as_batch(u)
+    if dev.is_device_tensor(lam):
+        ld = lam.to(device=ud.device, dtype=torch.float64)
+        if bool((ld < 0.0).any()):
+            raise DomainError("lambda must be >= 0")
+        lam_shape = tuple(ld.shape)
+    else:
+        lam_arr = np.asarray(lam, dtype=np.float64)
+        if np.any(lam_arr < 0.0):
+            raise DomainError("lambda must be >= 0")
+        lam_shape = lam_arr.shape
+        ld = dev.to_device(lam_arr.reshape(-1), torch.float64, ud.device)
+    if len(lam_shape) == 0:
+        ld = ld.reshape(1)
+    elif ld.numel() != ud.numel() or (host and lam_shape != np.shape(np.atleast_1d(np.asarray(u)))):
+        raise ConfigError("per-element lambda must match the shape of u")
+    od = torch.empty_like(ud)
+    kernels.ncchi2_eval(table.eval_stacks, table.nu, ud, ld.reshape(-1), od)
+    return _result(od, scalar, host, out)
+
+
+def evaluate(table, u, lam=None, dtype=np.float64, out=None):
+    """Evaluate any table type on a batch of uniforms (sampler.py:196-206)."""
+    if _is(table, "ConstantTable", ConstantTable):
+        return eval_constant(table, u, out=out)
+    if isinstance(table, SubDyadicTable):
+        return eval_subdyadic(table, u, out=out)
+    if _is(table, "DyadicPolyTable", DyadicPolyTable):
+        return eval_dyadic(table, u, dtype=dtype, out=out)
+    if _is(table, "NcChi2Table", NcChi2Table):
+        if lam is None:
+            raise ConfigError("non-central chi-squared tables need lam")
+        return eval_ncchi2(table, u, lam, out=out)
+    raise ConfigError(f"cannot evaluate object of type {type(table).__name__}")
+
+
+def _is(obj, name, cls) -> bool:
+    """isinstance, also accepting the reference's own table classes by name."""
+    return isinstance(obj, cls) or type(obj).__name__ == name
+
+
+def gaussian_inv_cdf(u, out=None):
+    """Exact AS241 quantile on the device (exact_dist.py:87-126), validating u."""
+    ud, scalar, host = _as_batch(u)
+    if ud.numel() and bool(((~torch.isfinite(ud)) | (ud <= 0.0) | (ud >= 1.0)).any()):
+        raise DomainError("gaussian_inv_cdf requires 0 < u < 1")
+    od = torch.empty_like(ud)
+    kernels.gaussian_inv_cdf(ud, od)
+    return _result(od, scalar, host, out)
+
+
+# ---------------------------------------------------------------------------
+# PCG32 stream and fused generators
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class CoupledGaussianBatch:
+    """Arrays of coupled samples; pair i derives from the same uniform (sampler.py:77-88)."""
+
+    z_exact: object
+    z_approx: object
+
+    def __len__(self) -> int:
+        return int(self.z_exact.shape[0])
+
+
+@dataclass
+class Pcg32Stream:
+    """Counter-addressable PCG32 stream on the device (the UniformStream analogue).
+
+    ``(seed, stream_id)`` = PCG32 ``(initstate, initseq)``; ``counter`` is the
+    index of the next 32-bit output.  f32 uniforms are ((w >> 9) + 0.5) 2^-23
+    (exact, open interval, never 1/2); f64 uniforms are (w + 0.5) 2^-32.
+    """
+
+    seed: int = 42
+    stream_id: int = 0
+    counter: int = 0
+
+    def __post_init__(self):
+        if not (0 <= int(self.seed) <= _MAX64 and 0 <= int(self.stream_id) < (1 << 63)):
+            raise ConfigError("seed must fit in 64 bits and stream_id in 63 bits")
+        if self.counter < 0:
+            raise ConfigError("counter must be >= 0")
+
+    # -- bookkeeping --------------------------------------------------------
+    def _take(self, n: int) -> int:
+        if n < 0:
+            raise ConfigError("cannot draw a negative number of words")
+        start = self.counter
+        self.counter = start + n
+        return start
+
+    def child(self, stream_id: int) -> "Pcg32Stream":
+        return Pcg32Stream(self.seed, stream_id)
+
+    def _out(self, out, n, dtype, device):
+        if out is None:
+            return torch.empty(n, dtype=dtype, device=device or dev.require_cuda())
+        if not (dev.is_device_tensor(out) and out.dtype == dtype and out.is_contiguous() and out.numel() == n):
+            raise ConfigError(f"out must be a contiguous CUDA {dtype} tensor of {n} elements")
+        return out
+
+    # -- raw draws ----------------------------------------------------------
+    def words(self, n: int, out=None, device=None) -> torch.Tensor:
+        start = self._take(n)
+        o = self._out(out, n, torch.uint32, device)
+        call("arv_pcg32_words", self.seed, self.stream_id, start, o.data_ptr(), n, dev.stream_handle(o.device))
+        return o
+
+    def uniforms(self, n: int, dtype=np.float32, out=None, device=None) -> torch.Tensor:
+        if dtype == np.float32:
+            start = self._take(n)
+            o = self._out(out, n, torch.float32, device)
+            call("arv_pcg32_uniform_f32", self.seed, self.stream_id, start, o.data_ptr(), n,
+                 dev.stream_handle(o.device))
+            return o
+        w = self.words(n, device=device)
+        u = (w.to(torch.int64).to(torch.float64) + 0.5) * 2.0**-32
+        if out is not None:
+            out.copy_(u)
+            return out
+        return u
+
+    # -- fused generators ---------------------------------------------------
+    def sample(self, table, n: int, out=None, device=None) -> torch.Tensor:
+        """n approximate Gaussian samples (f32) generated in one fused kernel.
+
+        ``table`` is a ConstantTable, DyadicPolyTable (reference layout),
+        SubDyadicTable, or the string ``"exact"`` (AS241 in f32 arithmetic).
+        """
+        o = self._out(out, n, torch.float32, device)
+        s = dev.stream_handle(o.device)
+        if _is(table, "ConstantTable", ConstantTable):
+            vals = dev.table_on_device(_values32(table), torch.float32, o.device)
+            q = int(vals.numel()).bit_length() - 1
+            start = self._take(n)
+            call("arv_pcg32_constant_f32", self.seed, self.stream_id, start, vals.data_ptr(), q, o.data_ptr(), n, s)
+        elif isinstance(table, SubDyadicTable):
+            c = dev.table_on_device(table.coeffs32, torch.float32, o.device)
+            start = self._take(n)
+            call("arv_pcg32_subdyadic_f32", self.seed, self.stream_id, start, c.data_ptr(), table.degree,
+                 table.n_octaves, table.sub_bits, o.data_ptr(), n, s)
+        elif _is(table, "DyadicPolyTable", DyadicPolyTable):
+            if getattr(table, "decay", 0.5) != 0.5:
+                raise ConfigError("the float32 fast path requires decay rate 1/2")
+            nat = _natural32(table)
+            c = dev.table_on_device(nat, torch.float32, o.device)
+            start = self._take(n)
+            call("arv_pcg32_subdyadic_f32", self.seed, self.stream_id, start, c.data_ptr(), table.degree,
+                 table.n_intervals, 0, o.data_ptr(), n, s)
+        elif table == "exact":
+            start = self._take(n)
+            call("arv_pcg32_gaussian_f32", self.seed, self.stream_id, start, o.data_ptr(), n, s)
+        else:
+            raise ConfigError(f"cannot sample from object of type {type(table).__name__}")
+        return o
+
+    def sample_exact64(self, n: int, out=None, device=None) -> torch.Tensor:
+        """AS241 in f64 of the same f32-lattice uniforms (exact comparator)."""
+        o = self._out(out, n, torch.float64, device)
+        start = self._take(n)
+        call("arv_pcg32_gaussian_f64", self.seed, self.stream_id, start, o.data_ptr(), n,
+             dev.stream_handle(o.device))
+        return o
+
+    def sample_host(self, table, n: int, out: np.ndarray | None = None) -> np.ndarray:
+        """Fused generation into a host buffer (the end-to-end path)."""
+        d = self.sample(table, n)
+        if out is None:
+            return d.cpu().numpy()
+        if isinstance(out, torch.Tensor):
+            out.copy_(d, non_blocking=True)
+            return out
+        np.copyto(out, d.cpu().numpy())
+        return out
+
+
+def _values32(table) -> np.ndarray:
+    v = getattr(table, "values32", None)
+    if v is None:
+        v = np.asarray(table.values, dtype=np.float32)
+        v.setflags(write=False)
+    return v
+
+
+_NAT_CACHE: dict = {}
+
+
+def _natural32(table) -> np.ndarray:
+    nat = getattr(table, "natural32", None)
+    if nat is not None:
+        return nat
+    key = id(table)
+    hit = _NAT_CACHE.get(key)
+    if hit is None or hit[0] is not table:
+        arr = np.ascontiguousarray(np.asarray(table.coeffs, dtype=np.float32)[:, 1:, None])
+        arr.setflags(write=False)
+        hit = (table, arr)
+        _NAT_CACHE[key] = hit
+    return hit[1]
+
+
+def sample_coupled(stream: Pcg32Stream, table, n: int) -> CoupledGaussianBatch:
+    """Draw n uniforms once; exact and approximate Gaussians (sampler.py:209-218)."""
+    u = stream.uniforms(n, dtype=np.float64)
+    z_exact = torch.empty_like(u)
+    kernels.gaussian_inv_cdf(u, z_exact)
+    z_approx = evaluate(table, u)
+    if isinstance(z_approx, torch.Tensor) and z_approx.dtype != torch.float64:
+        z_approx = z_approx.to(torch.float64)
+    return CoupledGaussianBatch(z_exact=z_exact, z_approx=z_approx)
+
+
+def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous [lo, hi) of ``n_total`` samples owned by ``rank`` (4-aligned)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ConfigError("bad rank/world")
+    groups = (n_total + 3) // 4
+    per = groups // world
+    extra = groups % world
+    g_lo = rank * per + min(rank, extra)
+    g_hi = g_lo + per + (1 if rank < extra else 0)
+    return min(4 * g_lo, n_total), min(4 * g_hi, n_total)

@@ -1,0 +1,187 @@
+"""Pin the CPU oracle against the reference's own outputs (tests/golden).
+
+CPU only.  Every comparison of integer/index/f32 lattice work is bit-exact;
+AS241 tails (numpy log vs libm log) use a stated ulp-level tolerance.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+# Published pcg32 demo (pcg-c-basic, pcg32_srandom_r(42, 54)): first outputs.
+PCG32_DEMO_42_54 = [0xA15C02B7, 0x7B47F409, 0xBA1D3330, 0x83D2F293, 0xBFA4784B, 0xCBED606E]
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint32 if a.dtype == np.float32 else np.uint64)
+
+
+class TestPcg32:
+    def test_published_demo_sequence(self, orc, golden):
+        assert list(orc.pcg32_words(42, 54, 0, 6)) == PCG32_DEMO_42_54
+        assert list(golden["pcg_kat_42_54"]) == PCG32_DEMO_42_54
+
+    def test_c_matches_pure_python(self, orc, golden):
+        assert np.array_equal(orc.pcg32_words(42, 0, 0, 4096), golden["pcg_words_42_0"])
+        assert np.array_equal(orc.pcg32_words(7, 3, 100, 200), golden["pcg_words_7_3_off"])
+
+    @pytest.mark.parametrize("offset", [0, 1, 3, 4, 1000, 123457])
+    def test_jump_ahead_is_offset(self, orc, offset):
+        full = orc.pcg32_words(9, 11, 0, offset + 64)
+        assert np.array_equal(orc.pcg32_words(9, 11, offset, 64), full[offset:])
+
+    def test_jump_composition(self, orc):
+        _, inc = orc.pcg32_seed(1, 2)
+        a1, c1 = orc.lcg_jump(12345, inc)
+        a2, c2 = orc.lcg_jump(67890, inc)
+        a, c = orc.lcg_jump(12345 + 67890, inc)
+        m = (1 << 64) - 1
+        assert a == (a2 * a1) & m and c == (a2 * c1 + c2) & m
+
+    def test_lattice_mapping(self, orc, golden):
+        u = orc.u32_to_f32(golden["lattice_words"])
+        assert np.array_equal(bits(u), bits(golden["lattice_u32"]))
+        assert u.min() > 0 and u.max() < 1 and not np.any(u == 0.5)
+        k = golden["lattice_words"] >> np.uint32(9)
+        assert np.array_equal(u.astype(np.float64), (k.astype(np.float64) + 0.5) * 2.0**-23)
+
+
+class TestPluginKernels:
+    def test_constant_eval(self, orc, golden, tables_npz):
+        v = tables_npz["constant_q10_l1"]
+        out = orc.constant_eval(v, golden["lattice_u32"].astype(np.float64))
+        assert np.array_equal(bits(out), bits(golden["const_q10_out"]))
+        out = orc.constant_eval(v, golden["u64"])
+        assert np.array_equal(bits(out), bits(golden["constant_u64_out"]))
+
+    def test_constant_index_is_top_bits(self, golden, tables_npz):
+        v = tables_npz["constant_q10_l1"]
+        w = golden["lattice_words"]
+        assert np.array_equal(golden["const_q10_out"], v[w >> np.uint32(22)])
+
+    @pytest.mark.parametrize("name", ["dyadic_linear_k15", "dyadic_cubic_k15"])
+    def test_dyadic_eval32(self, orc, golden, tables_npz, name):
+        out = orc.dyadic_eval32(tables_npz[name].astype(np.float32), golden["lattice_u32"])
+        assert np.array_equal(bits(out), bits(golden[f"{name}_eval32_out"]))
+
+    @pytest.mark.parametrize("name", ["dyadic_linear_k15", "dyadic_cubic_k15"])
+    def test_dyadic_eval64(self, orc, golden, tables_npz, name):
+        out = orc.dyadic_eval(tables_npz[name], golden["u64"])
+        assert np.array_equal(bits(out), bits(golden[f"{name}_eval_out"]))
+
+    def test_dyadic_indices(self, orc, golden):
+        assert np.array_equal(orc.dyadic_index(golden["u64"], 15), golden["dyadic_index_cap15"])
+        v = np.minimum(golden["u64"], 1.0 - golden["u64"])
+        assert np.array_equal(orc.dyadic_index(v, 1 << 62), golden["dyadic_index_uncapped"])
+        assert np.array_equal(orc.dyadic_index(golden["pow2"], 64), golden["pow2_index"])
+        assert np.array_equal(orc.dyadic_index32(golden["lattice_u32"], 15), golden["dyadic32_index_out"])
+        assert np.array_equal(orc.dyadic_index32(golden["index32_probe"], 15), golden["index32_probe_out"])
+
+    def test_ncchi2_eval(self, orc, golden, tables_npz):
+        st, nu = tables_npz["ncchi2_cir_k64_stacks"], float(tables_npz["ncchi2_cir_k64_nu"])
+        out = orc.ncchi2_eval(st, nu, golden["ncchi2_u"], golden["ncchi2_lam"])
+        assert np.array_equal(bits(out), bits(golden["ncchi2_k64_perelem_out"]))
+        out = orc.ncchi2_eval(st, nu, golden["ncchi2_u"], np.array([7.5]))
+        assert np.array_equal(bits(out), bits(golden["ncchi2_k64_shared_out"]))
+
+    def test_as241(self, orc, golden):
+        u = golden["as241_u"]
+        ref = golden["as241_out"]
+        out = orc.as241_f64(u)
+        central = np.abs(u - 0.5) <= 0.425
+        # central branch: identical operation sequence, no transcendental -> bit-exact
+        assert np.array_equal(bits(out[central]), bits(ref[central]))
+        # tails depend on log (numpy SIMD vs libm, each <= 1 ulp): relative 1e-14
+        np.testing.assert_allclose(out[~central], ref[~central], rtol=1e-14, atol=0)
+
+
+class TestFusedAndFullSize:
+    def test_fused_constant_matches_reference(self, orc, golden, tables_npz):
+        n = 1 << 14
+        out = orc.pcg32_constant_f32(42, 0, 0, tables_npz["constant_q10_l1"], n)
+        assert np.array_equal(bits(out), bits(golden["const_q10_out"][:n].astype(np.float32)))
+
+    def test_config1_full_hash(self, orc, hashes, tables_npz):
+        out = orc.pcg32_constant_f32(42, 0, 0, tables_npz["constant_q10_l1"], 1 << 24)
+        assert hashlib.sha256(out.tobytes()).hexdigest() == hashes["config1_const_q10_f32_sha256_2^24"]
+
+    def test_dyadic_k15_full_hash(self, orc, hashes, tables_npz):
+        out = orc.pcg32_dyadic_f32(42, 0, 0, tables_npz["dyadic_linear_k15"].astype(np.float32), 1 << 24)
+        assert hashlib.sha256(out.tobytes()).hexdigest() == hashes["dyadic_linear_k15_f32_sha256_2^24"]
+
+
+class TestSubDyadic:
+    def test_degenerate_table_equals_reference_dyadic(self, orc, golden, tables_npz):
+        """Sub-interval evaluator with K15 coefficients replicated over 8 slots
+        must reproduce the reference dyadic_eval32 bit for bit (index + arithmetic)."""
+        c = tables_npz["dyadic_linear_k15"].astype(np.float32)
+        deg = np.repeat(c[:, 1:, None], 8, axis=2)
+        out = orc.subdyadic_eval32(deg, 3, golden["lattice_u32"])
+        assert np.array_equal(bits(out), bits(golden["dyadic_linear_k15_eval32_out"]))
+        out = orc.pcg32_subdyadic_f32(42, 0, 0, deg, 3, 1 << 14)
+        assert np.array_equal(bits(out), bits(golden["dyadic_linear_k15_eval32_out"][: 1 << 14]))
+
+    def test_sub_interval_membership(self, orc, golden):
+        """Label each slot with its own id: the selected slot's interval contains v."""
+        K, b = 16, 3
+        ids = np.arange(K * 8, dtype=np.float32).reshape(K, 8)
+        c = np.stack([ids, np.zeros_like(ids)])  # z = id (c1 = 0)
+        u = golden["lattice_u32"]
+        z = orc.subdyadic_eval32(c, b, u)
+        e = np.abs(z).astype(np.int64)
+        j = e // 8 + 1
+        s = e % 8
+        v = np.minimum(u, np.float32(1) - u).astype(np.float64)
+        a = 2.0 ** -(j + 1)
+        lo = np.where(j < K, a + s * a / 8, 0.0)
+        hi = np.where(j < K, a + (s + 1) * a / 8, 2.0**-K)
+        assert np.all((lo <= v) & (v < hi))
+        assert np.all(s[j == K] == 0)
+
+    def test_shipped_table_error(self, orc, tables_npz):
+        c = tables_npz["subdyadic_linear_k16_s8"].astype(np.float32)
+        n = 1 << 20
+        a = orc.pcg32_subdyadic_f32(42, 0, 0, c, 3, n)
+        e = orc.pcg32_as241_f64(42, 0, 0, n)
+        rmse = float(np.sqrt(np.mean((a - e) ** 2)))
+        assert 2e-4 < rmse < 6e-4  # ~3.8e-4 (K15 reference layout: 6.4e-3)
+
+
+class TestMlmcRestatement:
+    def test_gbm_paths(self, orc, golden, hashes, tables_npz):
+        lin = tables_npz["dyadic_linear_k15"]
+        n = hashes["gbm_n_paths"]
+        for scheme, payoff, level, n0 in hashes["gbm_cases"]:
+            ref = golden[f"gbm_{scheme}_{payoff}_l{level}_n{n0}"]
+            got = np.stack(orc.gbm_paths(mu=0.05, sigma=0.2, x0=1.0, t_end=1.0, level=level, n0=n0,
+                                         milstein=scheme == "milstein", payoff_call=payoff == "call", strike=1.0,
+                                         coeffs=lin, seed=42, seq=level << 32, n_paths=n))
+            # approximate side: table + em_step only -> bit-exact
+            assert np.array_equal(bits(got[2:]), bits(ref[2:])), (scheme, payoff, level, n0)
+            # exact side goes through AS241 tails (log): relative 1e-13
+            np.testing.assert_allclose(got[:2], ref[:2], rtol=1e-13, atol=1e-15)
+
+    def test_cir_euler_paths(self, orc, golden, hashes, tables_npz):
+        lin = tables_npz["dyadic_linear_k15"]
+        for level, n0 in hashes["cir_euler_cases"]:
+            ref = golden[f"cir_euler_l{level}_n{n0}"]
+            got = np.stack(orc.cir_euler_paths(kappa=0.5, theta=0.04, sigma=0.2, x0=0.04, t_end=1.0, level=level,
+                                               n0=n0, payoff_call=False, strike=1.0, coeffs=lin, seed=42,
+                                               seq=(level << 32) | 5, n_paths=512))
+            assert np.array_equal(bits(got[2:]), bits(ref[2:]))
+            np.testing.assert_allclose(got[:2], ref[:2], rtol=1e-12, atol=1e-15)
+
+    def test_cir_exact_paths(self, golden, hashes, tables_npz):
+        from oracle import cir
+
+        st, nu_t = tables_npz["ncchi2_cir_k16_stacks"], float(tables_npz["ncchi2_cir_k16_nu"])
+        for level, n0 in hashes["cir_exact_cases"]:
+            ref = golden[f"cir_exact_l{level}_n{n0}"]
+            xe, xa, worst = cir.cir_exact_paths(kappa=0.5, theta=0.04, sigma=0.2, x0=0.04, t_end=1.0, level=level,
+                                                n0=n0, stacks=st, nu_table=nu_t, seed=42, seq=level << 32,
+                                                n_paths=256)
+            assert np.array_equal(bits(xa), bits(ref[1]))
+            np.testing.assert_allclose(xe, ref[0], rtol=1e-12)
+            assert worst <= 1e-8
