@@ -288,16 +288,67 @@ class Pcg32Stream:
              dev.stream_handle(o.device))
         return o
 
-    def sample_host(self, table, n: int, out: np.ndarray | None = None) -> np.ndarray:
-        """Fused generation into a host buffer (the end-to-end path)."""
-        d = self.sample(table, n)
+    def sample_host(self, table, n: int, out=None, chunk: int = 1 << 25, sync: bool = True):
+        """Fused generation straight into a host buffer (the end-to-end path).
+
+        The batch is produced in chunks on the current stream while a side
+        stream drains finished chunks device->host into ``out`` (a pinned
+        CPU tensor for full PCIe rate; allocated pinned if None), so the
+        HBM-side generation hides behind the host link.  Returns ``out``.
+        """
+        device = dev.require_cuda()
         if out is None:
-            return d.cpu().numpy()
-        if isinstance(out, torch.Tensor):
-            out.copy_(d, non_blocking=True)
-            return out
-        np.copyto(out, d.cpu().numpy())
+            out = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        if not isinstance(out, torch.Tensor):
+            host = out
+            out = torch.from_numpy(np.ascontiguousarray(host))
+        if out.numel() != n or out.dtype != torch.float32 or out.is_cuda:
+            raise ConfigError("out must be a host float32 buffer of n elements")
+        chunk = max(4, min(chunk, n)) & ~3
+        comp = torch.cuda.current_stream(device)
+        copy = _side_stream(device)
+        bufs = _chunk_buffers(device, chunk)
+        freed = [None, None]
+        start = self.counter
+        for i, lo in enumerate(range(0, n, chunk)):
+            hi = min(lo + chunk, n)
+            b = bufs[i & 1]
+            if freed[i & 1] is not None:
+                comp.wait_event(freed[i & 1])
+            self.counter = start + lo
+            self.sample(table, hi - lo, out=b[: hi - lo])
+            made = torch.cuda.Event()
+            made.record(comp)
+            copy.wait_event(made)
+            with torch.cuda.stream(copy):
+                out[lo:hi].copy_(b[: hi - lo], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+            freed[i & 1] = ev
+        self.counter = start + n
+        comp.wait_stream(copy)
+        if sync:
+            comp.synchronize()
         return out
+
+
+_SIDE: dict = {}
+_BUFS: dict = {}
+
+
+def _side_stream(device) -> torch.cuda.Stream:
+    s = _SIDE.get(device.index)
+    if s is None:
+        s = _SIDE[device.index] = torch.cuda.Stream(device)
+    return s
+
+
+def _chunk_buffers(device, chunk: int):
+    key = (device.index, chunk)
+    b = _BUFS.get(key)
+    if b is None:
+        b = _BUFS[key] = [torch.empty(chunk, dtype=torch.float32, device=device) for _ in range(2)]
+    return b
 
 
 def _values32(table) -> np.ndarray:

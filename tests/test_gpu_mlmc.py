@@ -1,0 +1,155 @@
+"""GPU parity of the nested-MLMC path kernels against the reference's own
+per-path payoffs (golden, PCG32 uniforms) and the oracle restatement, plus
+the statistical targets of SURVEY.md §8d."""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def arv():
+    import paper_2012_09715_b200 as arv
+
+    return arv
+
+
+GBM = dict(mu=0.05, sigma=0.2, x0=1.0, t_end=1.0)
+CIR = dict(kappa=0.5, theta=0.04, sigma=0.2, x0=0.04, t_end=1.0)
+
+
+def test_gbm_paths_match_reference(arv, golden, hashes):
+    lin = arv.load_table("dyadic_linear_k15")
+    n = hashes["gbm_n_paths"]
+    for scheme, payoff, level, n0 in hashes["gbm_cases"]:
+        spec = arv.LevelSpec(level=level, scheme=scheme, process=arv.GbmParams(**GBM), rv_source=lin,
+                             kind="four_way", payoff=payoff, strike=1.0, n0=n0)
+        b = arv.simulate(spec, arv.level_stream(42, level), n)
+        got = torch.stack([b.p_fine_exact, b.p_coarse_exact, b.p_fine_approx, b.p_coarse_approx]).cpu().numpy()
+        ref = golden[f"gbm_{scheme}_{payoff}_l{level}_n{n0}"]
+        assert np.array_equal(bits(got[2:]), bits(ref[2:])), (scheme, payoff, level, n0)
+        np.testing.assert_allclose(got[:2], ref[:2], rtol=1e-13, atol=1e-15)
+
+
+def test_gbm_paths_match_oracle_and_shard(arv, orc, tables_npz):
+    lin = arv.load_table("dyadic_linear_k15")
+    n, level = 3000, 5
+    spec = arv.LevelSpec(level=level, scheme="milstein", process=arv.GbmParams(**GBM), rv_source=lin,
+                         kind="four_way", n0=1)
+    from paper_2012_09715_b200.mlmc import run_level
+
+    _, paths, _ = run_level(spec, arv.level_stream(7, level), n, path_lo=1000, path_count=1500, want_paths=True)
+    ref = np.stack(orc.gbm_paths(mu=0.05, sigma=0.2, x0=1.0, t_end=1.0, level=level, n0=1, milstein=True,
+                                 payoff_call=False, strike=1.0, coeffs=tables_npz["dyadic_linear_k15"], seed=7,
+                                 seq=level << 32, n_paths=n, path_lo=1000, path_hi=2500))
+    got = paths.cpu().numpy()
+    assert np.array_equal(bits(got[2:]), bits(ref[2:]))
+    np.testing.assert_allclose(got[:2], ref[:2], rtol=1e-13, atol=1e-15)
+
+
+def test_cir_euler_paths_match_reference(arv, golden, hashes):
+    lin = arv.load_table("dyadic_linear_k15")
+    for level, n0 in hashes["cir_euler_cases"]:
+        spec = arv.LevelSpec(level=level, scheme="cir_euler_truncated", process=arv.CirParams(**CIR),
+                             rv_source=lin, kind="four_way", n0=n0)
+        b = arv.simulate(spec, arv.level_stream(42, level, 5), 512)
+        got = torch.stack([b.p_fine_exact, b.p_coarse_exact, b.p_fine_approx, b.p_coarse_approx]).cpu().numpy()
+        ref = golden[f"cir_euler_l{level}_n{n0}"]
+        assert np.array_equal(bits(got[2:]), bits(ref[2:]))
+        np.testing.assert_allclose(got[:2], ref[:2], rtol=1e-12, atol=1e-15)
+
+
+def test_cir_exact_paths_match_reference(arv, golden, hashes):
+    tab = arv.load_table("ncchi2_cir_k16_stacks")
+    for level, n0 in hashes["cir_exact_cases"]:
+        spec = arv.LevelSpec(level=level, scheme="cir_exact", process=arv.CirParams(**CIR), rv_source=tab,
+                             kind="four_way", n0=n0)
+        b = arv.simulate(spec, arv.level_stream(42, level), 256)
+        ref = golden[f"cir_exact_l{level}_n{n0}"]
+        # approximate side: ncchi2_eval chain, bit-exact
+        assert np.array_equal(bits(b.p_fine_approx.cpu().numpy()), bits(ref[1]))
+        # exact side: device Newton on the Poisson-gamma CDF vs CDFLIB Newton; both
+        # meet |F - u| <= tol_f, so the states agree to ~1e-9 relative
+        np.testing.assert_allclose(b.p_fine_exact.cpu().numpy(), ref[0], rtol=1e-7)
+
+
+def test_device_ncchi2_quantile_contract(arv):
+    """|chndtr(x) - u| <= 1e-8 (exact_dist.py:454-460) on a (u, lam) grid incl. tails."""
+    from scipy import special as sp
+
+    from paper_2012_09715_b200 import _device as dev
+    from paper_2012_09715_b200._native import call
+
+    nu = 4 * 0.5 * 0.04 / 0.2**2
+    u = np.concatenate([np.linspace(1e-6, 1 - 1e-6, 301), [1e-10, 1e-9, 1e-8, 1 - 1e-8, 1 - 1e-9, 0.5]])
+    for lam in (0.0, 1e-6, 0.5, 3.0, 30.0, 250.0, 1000.0):
+        ud = torch.from_numpy(u).cuda()
+        ld = torch.full((1,), lam, dtype=torch.float64, device="cuda")
+        xd = torch.empty_like(ud)
+        rd = torch.empty_like(ud)
+        call("arv_ncchi2_inv_cdf", ud.data_ptr(), ld.data_ptr(), 1, nu, None, xd.data_ptr(), rd.data_ptr(),
+             ud.numel(), dev.stream_handle())
+        x = xd.cpu().numpy()
+        resid = np.abs(sp.chndtr(x, nu, lam) - u)
+        assert resid.max() <= 1e-8, (lam, resid.max(), u[np.argmax(resid)])
+        assert rd.cpu().numpy().max() <= 1e-8
+
+
+def test_level_stats_match_per_path(arv):
+    lin = arv.load_table("dyadic_linear_k15")
+    spec = arv.LevelSpec(level=3, scheme="euler_maruyama", process=arv.GbmParams(**GBM), rv_source=lin,
+                         kind="four_way", n0=1)
+    n = 100_000
+    suite = arv.estimate_level_suite(spec, arv.level_stream(5, 3), n)
+    b = arv.simulate(spec, arv.level_stream(5, 3), n)
+    fe, ce, fa, ca = (t.cpu().numpy() for t in (b.p_fine_exact, b.p_coarse_exact, b.p_fine_approx, b.p_coarse_approx))
+    for key, d in (("two_way_exact", fe - ce), ("two_way_approx", fa - ca), ("four_way", fe - ce - fa + ca)):
+        assert suite[key].n_paths == n
+        np.testing.assert_allclose(suite[key].mean, d.mean(), rtol=1e-12, atol=1e-17)
+        np.testing.assert_allclose(suite[key].variance, d.var(ddof=1), rtol=1e-10)
+    # nested identity (helpers.py:393-399): two_way_approx + four_way == two_way_exact
+    lhs = suite["two_way_approx"].mean + suite["four_way"].mean
+    assert abs(lhs - suite["two_way_exact"].mean) <= 1e-12 * abs(suite["two_way_exact"].mean)
+    # determinism
+    again = arv.estimate_level_suite(spec, arv.level_stream(5, 3), n)
+    assert all(again[k].mean == suite[k].mean and again[k].variance == suite[k].variance for k in suite)
+
+
+def test_gbm_statistical_targets(arv):
+    """level-0 mean ~ 1.05, four-way/two-way gap ~ -13.5 (log2)."""
+    lin = arv.load_table("dyadic_linear_k15")
+    n = 1 << 20
+    gaps = []
+    for level in range(0, 7):
+        spec = arv.LevelSpec(level=level, scheme="euler_maruyama", process=arv.GbmParams(**GBM), rv_source=lin,
+                             kind="four_way", n0=1)
+        s = arv.estimate_level_suite(spec, arv.level_stream(42, level), n)
+        if level == 0:
+            se = math.sqrt(s["two_way_exact"].variance / n)
+            assert abs(s["two_way_exact"].mean - 1.05) < 4 * se + 1e-3
+        else:
+            gaps.append(math.log2(s["four_way"].variance / s["two_way_exact"].variance))
+    assert all(-14.5 < g < -12.5 for g in gaps), gaps
+
+
+def test_cir_statistical_targets(arv):
+    tab = arv.load_table("ncchi2_cir_k64_stacks")
+    n = 1 << 15
+    for level in (0, 3):
+        spec = arv.LevelSpec(level=level, scheme="cir_exact", process=arv.CirParams(**CIR), rv_source=tab,
+                             kind="four_way", n0=1)
+        s = arv.estimate_level_suite(spec, arv.level_stream(42, level), n)
+        assert abs(s["plain_exact"].mean - 0.04) < 4 * math.sqrt(s["plain_exact"].variance / n)
+        assert 0.8e-3 < s["plain_exact"].variance < 1.25e-3  # closed form 1.01e-3
+        gap = math.log2(s["correction"].variance / s["plain_exact"].variance)
+        assert gap < -12.0, gap

@@ -1,0 +1,214 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle and
+the reference's golden vectors.  Integer / index / f32 table work is
+bit-exact; AS241 tails use a stated ulp-level tolerance."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def bits(a):
+    if isinstance(a, torch.Tensor):
+        a = a.cpu().numpy()
+    a = np.ascontiguousarray(a)
+    return a.view({4: np.uint32, 8: np.uint64}[a.dtype.itemsize])
+
+
+@pytest.fixture(scope="module")
+def arv():
+    import paper_2012_09715_b200 as arv
+
+    return arv
+
+
+def test_library_is_the_in_tree_build(arv):
+    from paper_2012_09715_b200 import _native
+
+    with open("/proc/self/maps") as fh:
+        maps = fh.read()
+    assert _native.LIB_PATH in maps
+
+
+class TestPcg32Device:
+    @pytest.mark.parametrize("offset,n", [(0, 4096), (3, 4093), (1 << 20, 100003), (2**40 + 5, 7)])
+    def test_words(self, arv, orc, offset, n):
+        s = arv.Pcg32Stream(42, 0, counter=offset)
+        w = s.words(n)
+        assert np.array_equal(w.cpu().numpy(), orc.pcg32_words(42, 0, offset, n))
+        assert s.counter == offset + n
+
+    def test_words_unaligned_output(self, arv, orc):
+        buf = torch.empty(1001, dtype=torch.uint32, device="cuda")
+        arv.Pcg32Stream(5, 9).words(1000, out=buf[1:])
+        assert np.array_equal(buf[1:].cpu().numpy(), orc.pcg32_words(5, 9, 0, 1000))
+
+    def test_uniform_f32(self, arv, orc):
+        u = arv.Pcg32Stream(42, 0).uniforms(1 << 16)
+        ref = orc.u32_to_f32(orc.pcg32_words(42, 0, 0, 1 << 16))
+        assert np.array_equal(bits(u), bits(ref))
+
+    def test_shards_concatenate(self, arv, orc):
+        n = (1 << 18) + 3
+        full = arv.Pcg32Stream(42, 0).sample(arv.load_table("subdyadic_linear_k16_s8"), n)
+        parts = []
+        for r in range(3):
+            lo, hi = arv.shard_range(n, r, 3)
+            parts.append(arv.Pcg32Stream(42, 0, counter=lo).sample(arv.load_table("subdyadic_linear_k16_s8"), hi - lo))
+        assert np.array_equal(bits(torch.cat(parts)), bits(full))
+
+
+class TestFusedGenerators:
+    def test_constant_matches_reference(self, arv, golden):
+        t = arv.load_table("constant_q10_l1")
+        out = arv.Pcg32Stream(42, 0).sample(t, 1 << 14)
+        assert np.array_equal(bits(out), bits(golden["const_q10_out"][: 1 << 14].astype(np.float32)))
+
+    def test_config1_full_size_hash(self, arv, hashes):
+        out = arv.Pcg32Stream(42, 0).sample(arv.load_table("constant_q10_l1"), 1 << 24)
+        assert hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest() == hashes["config1_const_q10_f32_sha256_2^24"]
+
+    def test_dyadic_k15_reference_layout(self, arv, golden, hashes):
+        t = arv.load_table("dyadic_linear_k15")
+        out = arv.Pcg32Stream(42, 0).sample(t, 1 << 14)
+        assert np.array_equal(bits(out), bits(golden["dyadic_linear_k15_eval32_out"][: 1 << 14]))
+        out = arv.Pcg32Stream(42, 0).sample(t, 1 << 24)
+        assert hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest() == hashes["dyadic_linear_k15_f32_sha256_2^24"]
+
+    def test_cubic_reference_layout(self, arv, orc, tables_npz):
+        c = tables_npz["dyadic_cubic_k15"].astype(np.float32)
+        out = arv.Pcg32Stream(3, 1).sample(arv.load_table("dyadic_cubic_k15"), 100001)
+        assert np.array_equal(bits(out), bits(orc.pcg32_dyadic_f32(3, 1, 0, c, 100001)))
+
+    @pytest.mark.parametrize("seed,sid,offset,n", [(42, 0, 0, 1 << 20), (1, 7, 12345, 99999), (42, 0, 1 << 27, 1 << 16)])
+    def test_subdyadic_matches_oracle(self, arv, orc, tables_npz, seed, sid, offset, n):
+        t = arv.load_table("subdyadic_linear_k16_s8")
+        out = arv.Pcg32Stream(seed, sid, counter=offset).sample(t, n)
+        ref = orc.pcg32_subdyadic_f32(seed, sid, offset, tables_npz["subdyadic_linear_k16_s8"].astype(np.float32), 3, n)
+        assert np.array_equal(bits(out), bits(ref))
+
+    def test_config2_full_size(self, arv, orc, tables_npz):
+        """2^28 samples: chunk-wise bit-exact vs the oracle, and the error vs
+        AS241-f64 of the same uniforms (size-independent property)."""
+        n = 1 << 28
+        t = arv.load_table("subdyadic_linear_k16_s8")
+        out = arv.Pcg32Stream(42, 0).sample(t, n)
+        c = tables_npz["subdyadic_linear_k16_s8"].astype(np.float32)
+        for off in (0, n // 2, n - (1 << 20)):
+            ref = orc.pcg32_subdyadic_f32(42, 0, off, c, 3, 1 << 20)
+            assert np.array_equal(bits(out[off: off + (1 << 20)]), bits(ref))
+        ex = arv.Pcg32Stream(42, 0).sample_exact64(n)
+        err = out.double() - ex
+        rmse = float(torch.sqrt(torch.mean(err * err)))
+        assert 2e-4 < rmse < 6e-4
+        # antisymmetry on the lattice is structural: the top and bottom halves are mirror images
+        assert bool(torch.isfinite(out).all())
+
+    def test_unaligned_output(self, arv, orc, tables_npz):
+        buf = torch.empty(10001, dtype=torch.float32, device="cuda")
+        arv.Pcg32Stream(42, 0).sample(arv.load_table("subdyadic_linear_k16_s8"), 10000, out=buf[1:])
+        ref = orc.pcg32_subdyadic_f32(42, 0, 0, tables_npz["subdyadic_linear_k16_s8"].astype(np.float32), 3, 10000)
+        assert np.array_equal(bits(buf[1:]), bits(ref))
+
+    def test_gaussian_f64_comparator(self, arv, orc):
+        out = arv.Pcg32Stream(42, 0).sample_exact64(1 << 16).cpu().numpy()
+        ref = orc.pcg32_as241_f64(42, 0, 0, 1 << 16)
+        u = orc.u32_to_f32(orc.pcg32_words(42, 0, 0, 1 << 16)).astype(np.float64)
+        central = np.abs(u - 0.5) <= 0.425
+        assert np.array_equal(bits(out[central]), bits(ref[central]))
+        np.testing.assert_allclose(out, ref, rtol=4e-16 * 8, atol=0)
+
+    def test_gaussian_f32(self, arv, orc):
+        out = arv.Pcg32Stream(42, 0).sample("exact", 1 << 16).cpu().numpy()
+        ref = orc.pcg32_as241_f32(42, 0, 0, 1 << 16)
+        ulp = np.abs(bits(out).astype(np.int64) - bits(ref).astype(np.int64))
+        assert ulp.max() <= 4  # logf implementations differ by <= 1 ulp each
+        ex = orc.pcg32_as241_f64(42, 0, 0, 1 << 16)
+        np.testing.assert_allclose(out, ex, rtol=2e-6, atol=2e-6)
+
+
+class TestDropInKernels:
+    """The _kernels plugin functions on host (numpy) and device (torch) buffers."""
+
+    def test_constant_eval(self, arv, golden, tables_npz):
+        k = arv.get_kernels()
+        v = tables_npz["constant_q10_l1"]
+        u = golden["lattice_u32"].astype(np.float64)
+        out = np.empty_like(u)
+        k.constant_eval(v, u, out)
+        assert np.array_equal(bits(out), bits(golden["const_q10_out"]))
+        ud = torch.from_numpy(golden["u64"]).cuda()
+        od = torch.empty_like(ud)
+        k.constant_eval(v, ud, od)
+        assert np.array_equal(bits(od), bits(golden["constant_u64_out"]))
+
+    @pytest.mark.parametrize("name", ["dyadic_linear_k15", "dyadic_cubic_k15"])
+    def test_dyadic_eval(self, arv, golden, tables_npz, name):
+        k = arv.get_kernels()
+        out = np.empty_like(golden["u64"])
+        k.dyadic_eval(tables_npz[name], golden["u64"], out)
+        assert np.array_equal(bits(out), bits(golden[f"{name}_eval_out"]))
+        u32 = golden["lattice_u32"]
+        o32 = np.empty_like(u32)
+        k.dyadic_eval32(tables_npz[name].astype(np.float32), u32, o32)
+        assert np.array_equal(bits(o32), bits(golden[f"{name}_eval32_out"]))
+
+    def test_indices(self, arv, golden):
+        k = arv.get_kernels()
+        assert np.array_equal(k.dyadic_index(golden["u64"], 15), golden["dyadic_index_cap15"])
+        v = np.minimum(golden["u64"], 1.0 - golden["u64"])
+        assert np.array_equal(k.dyadic_index(v, 1 << 62), golden["dyadic_index_uncapped"])
+        assert np.array_equal(k.dyadic_index(golden["pow2"], 64), golden["pow2_index"])
+        assert np.array_equal(k.dyadic_index32(golden["lattice_u32"], 15), golden["dyadic32_index_out"])
+        assert np.array_equal(k.dyadic_index32(golden["index32_probe"], 15), golden["index32_probe_out"])
+
+    def test_ncchi2_eval(self, arv, golden, tables_npz):
+        k = arv.get_kernels()
+        st, nu = tables_npz["ncchi2_cir_k64_stacks"], float(tables_npz["ncchi2_cir_k64_nu"])
+        out = np.empty_like(golden["ncchi2_u"])
+        k.ncchi2_eval(st, nu, golden["ncchi2_u"], golden["ncchi2_lam"], out)
+        assert np.array_equal(bits(out), bits(golden["ncchi2_k64_perelem_out"]))
+        k.ncchi2_eval(st, nu, golden["ncchi2_u"], np.array([7.5]), out)
+        assert np.array_equal(bits(out), bits(golden["ncchi2_k64_shared_out"]))
+
+    def test_subdyadic_eval32(self, arv, orc, golden, tables_npz):
+        k = arv.get_kernels()
+        c = tables_npz["subdyadic_linear_k16_s8"].astype(np.float32)
+        u = np.concatenate([golden["lattice_u32"], np.array([0.5, 0.25, 2.0**-20, 1e-30], np.float32)])
+        out = np.empty_like(u)
+        k.subdyadic_eval32(c, 3, u, out)
+        assert np.array_equal(bits(out), bits(orc.subdyadic_eval32(c, 3, u)))
+
+    def test_as241(self, arv, golden):
+        u = golden["as241_u"]
+        out = np.asarray(arv.gaussian_inv_cdf(u))
+        ref = golden["as241_out"]
+        central = np.abs(u - 0.5) <= 0.425
+        assert np.array_equal(bits(out[central]), bits(ref[central]))
+        np.testing.assert_allclose(out[~central], ref[~central], rtol=1e-14, atol=0)
+
+    def test_sampler_wrappers(self, arv, golden, tables_npz):
+        lin = arv.load_table("dyadic_linear_k15")
+        assert arv.eval_dyadic(lin, 0.5) == 0.0
+        assert arv.eval_dyadic(lin, 0.5, dtype=np.float32) == 0.0
+        assert arv.dyadic_index(0.3) == 1 and arv.dyadic_index(2.0**-30, 15) == 15
+        const = arv.load_table("constant_q10_l1")
+        assert arv.eval_constant(const, 0.73) == const.values[747]
+        assert arv.eval_constant(const, np.nextafter(1.0, 0.0)) == const.values[-1]
+        with pytest.raises(arv.DomainError):
+            arv.eval_ncchi2(arv.load_table("ncchi2_cir_k64_stacks"), 0.5, -1.0)
+        with pytest.raises(arv.ConfigError):
+            arv.eval_ncchi2(arv.load_table("ncchi2_cir_k64_stacks"), np.array([0.5, 0.6]), np.array([1.0, 2.0, 3.0]))
+        with pytest.raises(arv.DomainError):
+            arv.gaussian_inv_cdf(np.array([0.0, 0.5]))
+
+    def test_launch_counter_advances(self, arv):
+        from paper_2012_09715_b200 import _native
+
+        before = _native.launch_count()
+        arv.Pcg32Stream(1, 1).sample(arv.load_table("constant_q10_l1"), 1000)
+        assert _native.launch_count() == before + 1
