@@ -107,8 +107,18 @@ ARV_API int arv_pcg32_gaussian_f64(uint64_t seed, uint64_t stream_id, uint64_t o
                            void *stream);
 ARV_API int arv_pcg32_gaussian_f32(uint64_t seed, uint64_t stream_id, uint64_t offset, float *out, int64_t n,
                            void *stream);
-/* Write-only bandwidth probe (st.global.v4 of a constant): the store roof. */
+/* Write-only bandwidth probes (streaming stores of a constant): the store
+ * roof.  mode 4 = st.global.cs.v4, 8 = st.global.cs.v8 (256-bit), 5 =
+ * st.global.v4; arv_store_probe = mode 8.  n % 8 == 0, out 32-byte aligned. */
 ARV_API int arv_store_probe(float *out, int64_t n, void *stream);
+ARV_API int arv_store_probe_ex(float *out, int64_t n, int mode, void *stream);
+
+/* Launch-shape knobs of the fused generators (process-wide):
+ * ARV_TUNE_GROUP = samples per thread-group, 4 (v4 stores) or 8 (v8, default);
+ * ARV_TUNE_CTAS_PER_SM = resident 256-thread CTAs per SM (default 8). */
+#define ARV_TUNE_GROUP 1
+#define ARV_TUNE_CTAS_PER_SM 2
+ARV_API int arv_set_tuning(int key, int value);
 
 /* ---- nested MLMC level kernels ------------------------------------------
  * Path p of a level uses PCG32 outputs k*n_paths_total + p (fine step k) of

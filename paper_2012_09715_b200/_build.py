@@ -44,8 +44,10 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(verbose_ptxas: bool = False, force: bool = False) -> str:
-    if not force and not needs_build():
+def build(verbose_ptxas: bool = False, force: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile every csrc/*.cu and link libarv_b200.so (or `out` with extra -D defines)."""
+    target = out or LIB_PATH
+    if not force and not defines and out is None and not needs_build():
         return LIB_PATH
     nvcc = nvcc_path()
     objdir = os.path.join(PKG_DIR, "build")
@@ -56,6 +58,10 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> str:
     ]
     if verbose_ptxas:
         common += ["-Xptxas", "-v"]
+    common += [f"-D{d}" for d in defines]
+    if defines or out is not None:
+        objdir = os.path.join(objdir, os.path.basename(target))
+        os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
@@ -65,10 +71,10 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> str:
     bad = [p.args[-3] for p in procs if p.wait() != 0]
     if bad:
         raise RuntimeError(f"nvcc failed for {bad}")
-    tmp = LIB_PATH + ".tmp"
+    tmp = target + ".tmp"
     subprocess.run([nvcc, *ARCH_FLAGS, "-shared", "-o", tmp, *objs], check=True)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

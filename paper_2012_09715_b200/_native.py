@@ -52,6 +52,8 @@ _SIGNATURES = {
     "arv_pcg32_gaussian_f64": ([_u64, _u64, _u64, _p, _i64, _p], _int),
     "arv_pcg32_gaussian_f32": ([_u64, _u64, _u64, _p, _i64, _p], _int),
     "arv_store_probe": ([_p, _i64, _p], _int),
+    "arv_store_probe_ex": ([_p, _i64, _int, _p], _int),
+    "arv_set_tuning": ([_int, _int], _int),
     "arv_mlmc_workspace_bytes": ([_i64], _i64),
     "arv_mlmc_gaussian_level": ([C.POINTER(LevelSpec), _p, _int, _i64, _p, _p, _p, _i64, _p], _int),
     "arv_mlmc_cir_exact_level": ([C.POINTER(LevelSpec), _p, _i64, _int, _i64, _dbl, _p, _p, _p, _p, _i64, _p], _int),
@@ -63,7 +65,8 @@ EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
 
 def _load() -> C.CDLL:
-    path = _build.LIB_PATH
+    # ARV_LIB_PATH: an alternative build of the same library (tuning experiments only)
+    path = os.environ.get("ARV_LIB_PATH") or _build.LIB_PATH
     if not os.path.exists(path):
         if os.environ.get("ARV_NO_AUTOBUILD"):
             raise ImportError(f"{path} is missing; run `python -m paper_2012_09715_b200._build`")
@@ -79,7 +82,7 @@ def _load() -> C.CDLL:
 
 
 lib = _load()
-LIB_PATH = _build.LIB_PATH
+LIB_PATH = os.environ.get("ARV_LIB_PATH") or _build.LIB_PATH
 
 
 def call(name: str, *args) -> None:

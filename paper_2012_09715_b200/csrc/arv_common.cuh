@@ -59,6 +59,33 @@ __host__ __device__ inline StreamStart pcg32_start(uint64_t seed, uint64_t strea
     return {j.a * s + j.c, inc};
 }
 
+// s' = a s + c (mod 2^64): IMAD.WIDE (low product + 64-bit addend), the two
+// cross terms into the high word, and their sum.
+__device__ __forceinline__ uint64_t lcg_step(uint64_t s, uint64_t a, uint64_t c) { return a * s + c; }
+
+// Opaque copy: stops ptxas from folding a kernel-parameter constant into
+// uniform registers (IMAD.WIDE cannot take a uniform 64-bit addend).
+__device__ __forceinline__ uint64_t as_register(uint64_t x) {
+    uint64_t r;
+    asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(x));
+    return r;
+}
+
+// a * b + c on the FMA pipe (IMAD), keeping the ALU pipe free.
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
+// ld.shared.f32 at a shared-space byte address plus an immediate offset.
+template <int OFF>
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(OFF));
+    return v;
+}
+
 // XSH-RR output of a state (the value produced *before* stepping).
 __device__ __forceinline__ uint32_t pcg32_output(uint64_t old) {
     const uint32_t lo = static_cast<uint32_t>(old);

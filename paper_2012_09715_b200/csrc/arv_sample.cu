@@ -1,13 +1,14 @@
 // Fused PCG32 -> inverse-CDF generators.
 //
-// One thread owns a PCG32 state in registers and produces groups of four
-// consecutive samples 4g..4g+3 (g = its group index), so each warp store is a
-// fully coalesced 512-byte st.global.v4; the only HBM traffic is the output.
+// One thread owns a PCG32 state in registers and produces groups of G = 4 or
+// 8 consecutive samples (G*g .. G*g+G-1 for its group index g), written with
+// one st.global.v4 (128-bit) or st.global.v8 (256-bit, sm_100) per group, so
+// every warp store is fully coalesced and the only HBM traffic is the output.
 // Within a group the LCG steps once per sample; between groups the thread
-// jumps over the 4(T-1) samples the other T-1 threads own with one affine
-// map (A, C) = LCG^(4T-3), precomputed on the host.  Output i of the call is
-// PCG32 output (offset + i) of stream (seed, stream_id) whatever the grid,
-// so shards on different GPUs concatenate bit-exactly.
+// jumps over the G(T-1) samples the other T-1 threads own with one affine
+// map (A, C) = LCG^(G T - G + 1), precomputed on the host.  Output i of a
+// call is PCG32 output (offset + i) of stream (seed, stream_id) whatever the
+// grid or G, so shards on different GPUs concatenate bit-exactly.
 //
 // Evaluators (reference semantics, see oracle/oracle.c):
 //   constant   values[floor(2^q u)]            (_kernels.pyx:16-23)
@@ -17,71 +18,123 @@
 
 namespace arv {
 
+// ------------------------------------------------------------ tuning ----
+// Compile-time variants (tools/prof_kernels.py builds them for sweeps):
+//   ARV_GEN_MINB    min resident CTAs per SM for __launch_bounds__ (register cap)
+//   ARV_GEN_UNROLL  groups per loop iteration
+// Sweep (B200, 2^28 samples, r01): MINB 6 / UNROLL 2 / group 8 / 8 CTAs per
+// SM was fastest for the sub-interval generator (0.206 ms vs 0.224-0.243 ms
+// for the other variants, incl. split half-chains).
+#ifndef ARV_GEN_MINB
+#define ARV_GEN_MINB 6
+#endif
+#ifndef ARV_GEN_UNROLL
+#define ARV_GEN_UNROLL 2
+#endif
+constexpr int kGenUnroll = ARV_GEN_UNROLL;
+// Process-wide launch shape knobs (arv_set_tuning); defaults from sweeps.
+static int g_group = 8;        // samples per thread-group: 4 (v4) or 8 (v8)
+static int g_ctas_per_sm = 8;  // resident CTAs per SM (256 threads each)
+
 struct GenArgs {
     uint64_t s_base;  // state whose output is sample 0 of this call
     uint64_t inc;
-    Affine stride;    // LCG^(4T-3)
+    Affine stride;    // LCG^(G T - G + 1)
     int64_t n;
+    uint64_t zero;    // always 0: makes derived constants per-thread registers
+    uint32_t zero32;
 };
 
 static GenArgs make_gen_args(uint64_t seed, uint64_t stream_id, uint64_t offset, int64_t n,
-                             int64_t total_threads) {
+                             int64_t total_threads, int G) {
     const StreamStart st = pcg32_start(seed, stream_id, offset);
     GenArgs a;
     a.s_base = st.state;
     a.inc = st.inc;
-    a.stride = lcg_jump(4ull * static_cast<uint64_t>(total_threads) - 3ull, st.inc);
+    a.stride = lcg_jump(static_cast<uint64_t>(G) * static_cast<uint64_t>(total_threads) - (G - 1), st.inc);
     a.n = n;
+    a.zero = 0;
+    a.zero32 = 0;
     return a;
 }
 
-// Drive `eval(w) -> uint32 bits` over the call's samples with v4 stores.
-template <class Eval>
-__device__ __forceinline__ void gen_loop_v4(const GenArgs &a, uint32_t *__restrict__ out, const Eval &eval) {
-    const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t n_full = static_cast<uint64_t>(a.n) >> 2;
-    const Affine j0 = lcg_jump(4ull * g, a.inc);
-    uint64_t s = j0.a * a.s_base + j0.c;
-    const uint64_t inc = a.inc;
-    const Affine st = a.stride;
-    for (; g < n_full; g += T) {
-        const uint32_t w0 = pcg32_output(s);
-        s = s * kPcgMult + inc;
-        const uint32_t w1 = pcg32_output(s);
-        s = s * kPcgMult + inc;
-        const uint32_t w2 = pcg32_output(s);
-        s = s * kPcgMult + inc;
-        const uint32_t w3 = pcg32_output(s);
-        s = st.a * s + st.c;
-        uint4 r;
-        r.x = eval(w0);
-        r.y = eval(w1);
-        r.z = eval(w2);
-        r.w = eval(w3);
-        __stcs(reinterpret_cast<uint4 *>(out) + g, r);
+template <int G>
+struct VecOut;
+template <>
+struct VecOut<4> {
+    __device__ __forceinline__ static void store(uint32_t *p, const uint32_t (&r)[4]) {
+        __stcs(reinterpret_cast<uint4 *>(p), make_uint4(r[0], r[1], r[2], r[3]));
     }
-    const int rem = static_cast<int>(a.n & 3);
+};
+template <>
+struct VecOut<8> {
+    __device__ __forceinline__ static void store(uint32_t *p, const uint32_t (&r)[8]) {
+        asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]), "r"(r[1]),
+                     "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                     : "memory");
+    }
+};
+
+// Drive `eval(w) -> uint32 bits` over the call's samples with G-wide stores
+// (out must be 4*G-byte aligned).
+template <int G, class Eval>
+__device__ __forceinline__ void gen_loop_vec(const GenArgs &a, uint32_t *__restrict__ out, const Eval &eval) {
+    const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t n_full = static_cast<uint64_t>(a.n) / G;
+    const Affine j0 = lcg_jump(static_cast<uint64_t>(G) * g0, a.inc);
+    uint64_t s = j0.a * a.s_base + j0.c;
+    const uint64_t z = static_cast<uint64_t>(threadIdx.x) * a.zero;  // 0, but not provably uniform
+    const uint64_t inc = a.inc + z;
+    const Affine st{a.stride.a + z, a.stride.c + z};
+    // Trip count once; the loop runs on a 32-bit counter and a pointer bump.
+    const uint32_t iters = g0 < n_full ? static_cast<uint32_t>((n_full - g0 + T - 1) / T) : 0u;
+    uint32_t *p = out + G * g0;
+    const uint64_t step = G * T;
+#pragma unroll kGenUnroll
+    for (uint32_t it = 0; it < iters; ++it) {
+        uint32_t w[G];
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            w[i] = pcg32_output(s);
+            s = i < G - 1 ? lcg_step(s, kPcgMult, inc) : lcg_step(s, st.a, st.c);
+        }
+        uint32_t r[G];
+#pragma unroll
+        for (int i = 0; i < G; ++i) r[i] = eval(w[i]);
+        VecOut<G>::store(p, r);
+        p += step;
+    }
+    const uint64_t g = g0 + static_cast<uint64_t>(iters) * T;
+    const int rem = static_cast<int>(a.n % G);
     if (g == n_full && rem) {
         for (int i = 0; i < rem; ++i) {
-            out[4 * g + i] = eval(pcg32_output(s));
-            s = s * kPcgMult + inc;
+            out[G * g + i] = eval(pcg32_output(s));
+            s = lcg_step(s, kPcgMult, inc);
         }
     }
 }
 
 // Scalar-store variant for outputs that are not 16-byte aligned.
 template <class Eval>
-__device__ __forceinline__ void gen_loop_v1(uint64_t s_base, uint64_t inc, Affine strideT, int64_t n,
-                                            uint32_t *__restrict__ out, const Eval &eval) {
+__device__ __forceinline__ void gen_loop_v1(uint64_t s_base, uint64_t inc, int64_t n, uint32_t *__restrict__ out,
+                                            const Eval &eval) {
     const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const Affine j0 = lcg_jump(i, inc);
+    const Affine sT = lcg_jump(T, inc);
     uint64_t s = j0.a * s_base + j0.c;
     for (; i < static_cast<uint64_t>(n); i += T) {
         out[i] = eval(pcg32_output(s));
-        s = strideT.a * s + strideT.c;
+        s = lcg_step(s, sT.a, sT.c);
     }
+}
+
+// MODE: 1 = scalar stores (unaligned out), 4 = v4, 8 = v8.
+template <int MODE, class Eval>
+__device__ __forceinline__ void gen_dispatch(const GenArgs &a, uint32_t *out, const Eval &ev) {
+    if constexpr (MODE == 1) gen_loop_v1(a.s_base, a.inc, a.n, out, ev);
+    else gen_loop_vec<MODE>(a, out, ev);
 }
 
 // ------------------------------------------------------------ evaluators --
@@ -108,59 +161,73 @@ struct EvalConstant {
         return __float_as_uint(tab[idx]);
     }
 };
-// Octave x sub-interval, reversed table (row r = K - j, r = K is the zero
-// row of v = 1/2): entry = (bits(v) >> (23 - b)) - ((126 - K) << b),
-// clamped below at 0 (all octaves >= K share the singular row 0).
+
+// Octave x sub-interval on the f32 lattice.  v = min(u, 1-u) is built
+// exactly in the FP pipe:  f = as_float(0x3F000000 | (w >> 9)) = 1/2 + t 2^-24,
+// d = 2 (f - 3/4) + 2^-24 = u - 1/2 (exact, never 0), v = 1/2 - |d|.  The
+// sign of d is the reference predicate (u < 1/2 <=> d < 0).  On the lattice
+// v lies in [2^-24, 1/2), so its biased exponent E is 103..125 and
+// bits(v) >> (23 - b) = (E << b) | sub indexes a "lattice table" of
+// 23 << b entries per coefficient plane directly (the base offset 103 << b
+// is folded into the shared-memory base address); octaves j = 126 - E >= K
+// hold the singular polynomial.  Planes are separate f32 arrays at a fixed
+// stride (one address IMAD, immediate offsets), so the four most frequent
+// octaves (94% of samples) hit disjoint banks.
+constexpr int kLatticeE0 = 103;                   // exponent of 2^-24
+constexpr int kLatticeOct = 23;                   // octaves 1..23 on the f32 lattice
+constexpr int kLatticePlane = kLatticeOct << 5;   // plane stride (max sub_bits = 5)
+
 template <int DEG>
 struct EvalSubDyadic {
-    const float *tab;  // (DEG+1) planes of `plane` floats, or float2 pairs when DEG == 1
-    int shift, base, plane;
+    uint32_t base;  // shared-space byte address of plane 0, pre-offset by -4 (103 << b)
+    int shift;
+    uint32_t four;  // 4, held in a register so the address is one IMAD (FMA pipe)
     __device__ __forceinline__ uint32_t operator()(uint32_t w) const {
-        const Reflected r = reflect_u32(w);
-        const int e = max(static_cast<int>(__float_as_uint(r.v) >> shift) - base, 0);
-        float z;
-        if constexpr (DEG == 1) {
-            const float2 c = reinterpret_cast<const float2 *>(tab)[e];
-            z = __fadd_rn(__fmul_rn(c.y, r.v), c.x);
-        } else {
-            z = tab[DEG * plane + e];
+        const float f = __uint_as_float(0x3F000000u | (w >> 9));
+        const float d = __fmaf_rn(2.0f, __fadd_rn(f, -0.75f), 0x1p-24f);  // exact
+        const float v = __fadd_rn(0.5f, -fabsf(d));                       // exact
+        const uint32_t addr = mad_u32(__float_as_uint(v) >> shift, four, base);
+        float z = lds_f32<DEG * kLatticePlane * 4>(addr);
 #pragma unroll
-            for (int d = DEG - 1; d >= 0; --d) z = __fadd_rn(__fmul_rn(z, r.v), tab[d * plane + e]);
+        for (int k = DEG - 1; k >= 0; --k) {
+            float c;
+            switch (k) {  // immediate plane offsets
+                case 0: c = lds_f32<0>(addr); break;
+                case 1: c = lds_f32<1 * kLatticePlane * 4>(addr); break;
+                case 2: c = lds_f32<2 * kLatticePlane * 4>(addr); break;
+                case 3: c = lds_f32<3 * kLatticePlane * 4>(addr); break;
+                default: c = lds_f32<4 * kLatticePlane * 4>(addr); break;
+            }
+            z = __fadd_rn(__fmul_rn(z, v), c);  // separately rounded (no FMA): reference parity
         }
-        return __float_as_uint(z) ^ (r.m & 0x80000000u);
+        return __float_as_uint(z) ^ (~__float_as_uint(d) & 0x80000000u);
     }
 };
 
-// Stage the natural-layout table (DEG+1, K, nsub) into the reversed layout.
+// Stage natural-layout coeffs (DEG+1, K, nsub) into the lattice table.
 template <int DEG>
 __device__ __forceinline__ void stage_subdyadic(float *sm, const float *__restrict__ coeffs, int K, int b) {
     const int nsub = 1 << b;
-    const int plane = (K + 1) << b;
+    const int plane = kLatticeOct << b;
     for (int e = threadIdx.x; e < plane; e += blockDim.x) {
-        const int r = e >> b, s = e & (nsub - 1);
-        const int j = K - r;
-        for (int d = 0; d <= DEG; ++d) {
-            const float c = j == 0 ? 0.0f : __ldg(coeffs + (static_cast<int64_t>(d) * K + (j - 1)) * nsub + (j == K ? 0 : s));
-            if constexpr (DEG == 1) sm[2 * e + d] = c;
-            else sm[d * plane + e] = c;
-        }
+        const int E = kLatticeE0 + (e >> b), s = e & (nsub - 1);
+        const int j = 126 - E;  // octave 1..23
+        const int jj = j < K ? j : K;
+        const int ss = j < K ? s : 0;
+        for (int d = 0; d <= DEG; ++d)
+            sm[d * kLatticePlane + e] = __ldg(coeffs + (static_cast<int64_t>(d) * K + (jj - 1)) * nsub + ss);
     }
     __syncthreads();
 }
 
 // --------------------------------------------------------------- kernels --
-template <class Eval>
-__global__ void __launch_bounds__(256) k_gen_simple(GenArgs a, uint32_t *out, Eval eval) {
-    gen_loop_v4(a, out, eval);
-}
-template <class Eval>
-__global__ void __launch_bounds__(256) k_gen_simple_v1(uint64_t s_base, uint64_t inc, Affine strideT, int64_t n,
-                                                       uint32_t *out, Eval eval) {
-    gen_loop_v1(s_base, inc, strideT, n, out, eval);
+template <int MODE, class Eval>
+__global__ void __launch_bounds__(256, ARV_GEN_MINB) k_gen_simple(GenArgs a, uint32_t *out, Eval eval) {
+    gen_dispatch<MODE>(a, out, eval);
 }
 
-template <bool V4>
-__global__ void __launch_bounds__(256) k_pcg32_constant(GenArgs a, const float *__restrict__ values, int q,
+template <int MODE>
+__global__ void __launch_bounds__(256, ARV_GEN_MINB) k_pcg32_constant(GenArgs a, const float *__restrict__ values, int q,
                                                         int use_smem, uint32_t *out) {
     extern __shared__ float4 smem4[];
     float *sm = reinterpret_cast<float *>(smem4);
@@ -171,28 +238,16 @@ __global__ void __launch_bounds__(256) k_pcg32_constant(GenArgs a, const float *
         __syncthreads();
         tab = sm;
     }
-    EvalConstant ev{tab, q <= 23 ? 32 - q : -1};
-    if constexpr (V4) {
-        gen_loop_v4(a, out, ev);
-    } else {
-        const Affine sT = lcg_jump(static_cast<uint64_t>(gridDim.x) * blockDim.x, a.inc);
-        gen_loop_v1(a.s_base, a.inc, sT, a.n, out, ev);
-    }
+    gen_dispatch<MODE>(a, out, EvalConstant{tab, q <= 23 ? 32 - q : -1});
 }
 
-template <int DEG, bool V4>
-__global__ void __launch_bounds__(256) k_pcg32_subdyadic(GenArgs a, const float *__restrict__ coeffs, int K, int b,
+template <int DEG, int MODE>
+__global__ void __launch_bounds__(256, ARV_GEN_MINB) k_pcg32_subdyadic(GenArgs a, const float *__restrict__ coeffs, int K, int b,
                                                          uint32_t *out) {
-    extern __shared__ float4 smem4[];
-    float *sm = reinterpret_cast<float *>(smem4);
+    __shared__ float sm[(DEG + 1) * kLatticePlane];
     stage_subdyadic<DEG>(sm, coeffs, K, b);
-    EvalSubDyadic<DEG> ev{sm, 23 - b, (126 - K) << b, (K + 1) << b};
-    if constexpr (V4) {
-        gen_loop_v4(a, out, ev);
-    } else {
-        const Affine sT = lcg_jump(static_cast<uint64_t>(gridDim.x) * blockDim.x, a.inc);
-        gen_loop_v1(a.s_base, a.inc, sT, a.n, out, ev);
-    }
+    const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sm)) - 4u * (kLatticeE0 << b);
+    gen_dispatch<MODE>(a, out, EvalSubDyadic<DEG>{base, 23 - b, 4u + threadIdx.x * a.zero32});
 }
 
 // f64 exact comparator: groups of 4 samples, two 16-byte stores.
@@ -207,7 +262,7 @@ __global__ void __launch_bounds__(256) k_pcg32_gauss64(GenArgs a, double *__rest
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             r[i] = as241_f64(static_cast<double>(u32_to_f32(pcg32_output(s))));
-            s = i < 3 ? s * kPcgMult + a.inc : a.stride.a * s + a.stride.c;
+            s = i < 3 ? lcg_step(s, kPcgMult, a.inc) : lcg_step(s, a.stride.a, a.stride.c);
         }
         double2 *o = reinterpret_cast<double2 *>(out + 4 * g);
         __stcs(o, make_double2(r[0], r[1]));
@@ -217,39 +272,57 @@ __global__ void __launch_bounds__(256) k_pcg32_gauss64(GenArgs a, double *__rest
     if (g == n_full && rem) {
         for (int i = 0; i < rem; ++i) {
             out[4 * g + i] = as241_f64(static_cast<double>(u32_to_f32(pcg32_output(s))));
-            s = s * kPcgMult + a.inc;
+            s = lcg_step(s, kPcgMult, a.inc);
         }
     }
 }
 
-__global__ void __launch_bounds__(256) k_store_probe(float4 *out, int64_t n4) {
+// Write-only roof probes: MODE 4 = st.global.cs.v4, 8 = st.global.cs.v8,
+// 5 = st.global.v4 (default eviction).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_store_probe(uint32_t *out, int64_t n) {
     const int64_t T = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    const float4 v = make_float4(1.f, 2.f, 3.f, 4.f);
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += T) __stcs(out + i, v);
+    constexpr int G = MODE == 8 ? 8 : 4;
+    uint32_t r[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) r[i] = 0x3F800000u + i;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n / G; i += T) {
+        if constexpr (MODE == 5)
+            *reinterpret_cast<uint4 *>(out + G * i) = make_uint4(r[0], r[1], r[2], r[3]);
+        else
+            VecOut<G>::store(out + G * i, r);
+    }
 }
 
 // ------------------------------------------------------------- launchers --
 constexpr int kGenBlock = 256;
-constexpr int kGenPerSM = 8;  // 2048 resident threads per SM
 
-static int gen_grid(int64_t n) { return stream_grid((n + 3) / 4, kGenBlock, kGenPerSM); }
+static bool aligned(const void *p, int bytes) { return (reinterpret_cast<uintptr_t>(p) & (bytes - 1)) == 0; }
 
-static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+// Store mode for an output pointer: the tuned group size if aligned for it.
+static int store_mode(const void *out) {
+    if (g_group == 8 && aligned(out, 32)) return 8;
+    if (aligned(out, 16)) return 4;
+    return 1;
+}
+
+static int gen_grid(int64_t n, int mode) {
+    return stream_grid((n + mode - 1) / mode, kGenBlock, g_ctas_per_sm);
+}
 
 template <class Eval>
 static int launch_simple(uint64_t seed, uint64_t sid, uint64_t offset, uint32_t *out, int64_t n, void *stream,
                          Eval ev, const char *what) {
     if (n < 0) return set_error(ARV_ERR_CONFIG, "%s: negative n", what);
     if (n == 0) return ARV_OK;
-    const int grid = gen_grid(n);
+    const int mode = store_mode(out);
+    const int grid = gen_grid(n, mode);
     const int64_t T = static_cast<int64_t>(grid) * kGenBlock;
-    const GenArgs a = make_gen_args(seed, sid, offset, n, T);
-    if (aligned16(out)) {
-        k_gen_simple<Eval><<<grid, kGenBlock, 0, as_stream(stream)>>>(a, out, ev);
-    } else {
-        const Affine sT = lcg_jump(static_cast<uint64_t>(T), a.inc);
-        k_gen_simple_v1<Eval><<<grid, kGenBlock, 0, as_stream(stream)>>>(a.s_base, a.inc, sT, n, out, ev);
-    }
+    const GenArgs a = make_gen_args(seed, sid, offset, n, T, mode == 1 ? 4 : mode);
+    cudaStream_t s = as_stream(stream);
+    if (mode == 8) k_gen_simple<8, Eval><<<grid, kGenBlock, 0, s>>>(a, out, ev);
+    else if (mode == 4) k_gen_simple<4, Eval><<<grid, kGenBlock, 0, s>>>(a, out, ev);
+    else k_gen_simple<1, Eval><<<grid, kGenBlock, 0, s>>>(a, out, ev);
     note_launch();
     return check_launch(what);
 }
@@ -259,6 +332,21 @@ static int launch_simple(uint64_t seed, uint64_t sid, uint64_t offset, uint32_t 
 using namespace arv;
 
 extern "C" {
+
+int arv_set_tuning(int key, int value) {
+    switch (key) {
+        case ARV_TUNE_GROUP:
+            if (value != 4 && value != 8) return set_error(ARV_ERR_CONFIG, "group must be 4 or 8");
+            g_group = value;
+            return ARV_OK;
+        case ARV_TUNE_CTAS_PER_SM:
+            if (value < 1 || value > 32) return set_error(ARV_ERR_CONFIG, "ctas_per_sm must be in [1, 32]");
+            g_ctas_per_sm = value;
+            return ARV_OK;
+        default:
+            return set_error(ARV_ERR_CONFIG, "unknown tuning key %d", key);
+    }
+}
 
 int arv_pcg32_words(uint64_t seed, uint64_t stream_id, uint64_t offset, uint32_t *out, int64_t n, void *stream) {
     return launch_simple(seed, stream_id, offset, out, n, stream, EvalWord{}, "arv_pcg32_words");
@@ -283,17 +371,22 @@ int arv_pcg32_constant_f32(uint64_t seed, uint64_t stream_id, uint64_t offset, c
     if (n == 0) return ARV_OK;
     const int use_smem = q <= 14;
     const size_t smem = use_smem ? (sizeof(float) << q) : 0;
-    const int grid = gen_grid(n);
+    const int mode = store_mode(out);
+    const int grid = gen_grid(n, mode);
     const int64_t T = static_cast<int64_t>(grid) * kGenBlock;
-    const GenArgs a = make_gen_args(seed, stream_id, offset, n, T);
+    const GenArgs a = make_gen_args(seed, stream_id, offset, n, T, mode == 1 ? 4 : mode);
     uint32_t *o = reinterpret_cast<uint32_t *>(out);
-    if (aligned16(out)) {
-        if (smem > 48 * 1024) cudaFuncSetAttribute(k_pcg32_constant<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_pcg32_constant<true><<<grid, kGenBlock, smem, as_stream(stream)>>>(a, values, q, use_smem, o);
-    } else {
-        if (smem > 48 * 1024) cudaFuncSetAttribute(k_pcg32_constant<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_pcg32_constant<false><<<grid, kGenBlock, smem, as_stream(stream)>>>(a, values, q, use_smem, o);
-    }
+    cudaStream_t s = as_stream(stream);
+#define ARV_CONST(M)                                                                                        \
+    do {                                                                                                    \
+        if (smem > 48 * 1024)                                                                               \
+            cudaFuncSetAttribute(k_pcg32_constant<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        k_pcg32_constant<M><<<grid, kGenBlock, smem, s>>>(a, values, q, use_smem, o);                        \
+    } while (0)
+    if (mode == 8) ARV_CONST(8);
+    else if (mode == 4) ARV_CONST(4);
+    else ARV_CONST(1);
+#undef ARV_CONST
     note_launch();
     return check_launch("arv_pcg32_constant_f32");
 }
@@ -305,17 +398,17 @@ int arv_pcg32_subdyadic_f32(uint64_t seed, uint64_t stream_id, uint64_t offset, 
     if (sub_bits < 0 || sub_bits > 5) return set_error(ARV_ERR_CONFIG, "sub_bits must be in [0, 5], got %d", sub_bits);
     if (n < 0) return set_error(ARV_ERR_CONFIG, "negative n");
     if (n == 0) return ARV_OK;
-    const size_t smem = sizeof(float) * (degree + 1) * ((size_t)(K + 1) << sub_bits);
-    const int grid = gen_grid(n);
+    const int mode = store_mode(out);
+    const int grid = gen_grid(n, mode);
     const int64_t T = static_cast<int64_t>(grid) * kGenBlock;
-    const GenArgs a = make_gen_args(seed, stream_id, offset, n, T);
+    const GenArgs a = make_gen_args(seed, stream_id, offset, n, T, mode == 1 ? 4 : mode);
     uint32_t *o = reinterpret_cast<uint32_t *>(out);
     cudaStream_t s = as_stream(stream);
-    const bool v4 = aligned16(out);
-#define ARV_SUB_CASE(D)                                                                         \
-    case D:                                                                                     \
-        if (v4) k_pcg32_subdyadic<D, true><<<grid, kGenBlock, smem, s>>>(a, coeffs, K, sub_bits, o); \
-        else k_pcg32_subdyadic<D, false><<<grid, kGenBlock, smem, s>>>(a, coeffs, K, sub_bits, o);   \
+#define ARV_SUB_CASE(D)                                                                               \
+    case D:                                                                                           \
+        if (mode == 8) k_pcg32_subdyadic<D, 8><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o);      \
+        else if (mode == 4) k_pcg32_subdyadic<D, 4><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o); \
+        else k_pcg32_subdyadic<D, 1><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o);                \
         break;
     switch (degree) {
         ARV_SUB_CASE(1)
@@ -332,22 +425,29 @@ int arv_pcg32_subdyadic_f32(uint64_t seed, uint64_t stream_id, uint64_t offset, 
 int arv_pcg32_gaussian_f64(uint64_t seed, uint64_t stream_id, uint64_t offset, double *out, int64_t n, void *stream) {
     if (n < 0) return set_error(ARV_ERR_CONFIG, "negative n");
     if (n == 0) return ARV_OK;
-    if (!aligned16(out)) return set_error(ARV_ERR_CONFIG, "arv_pcg32_gaussian_f64: out must be 16-byte aligned");
-    const int grid = gen_grid(n);
+    if (!aligned(out, 16)) return set_error(ARV_ERR_CONFIG, "arv_pcg32_gaussian_f64: out must be 16-byte aligned");
+    const int grid = stream_grid((n + 3) / 4, kGenBlock, g_ctas_per_sm);
     const int64_t T = static_cast<int64_t>(grid) * kGenBlock;
-    const GenArgs a = make_gen_args(seed, stream_id, offset, n, T);
+    const GenArgs a = make_gen_args(seed, stream_id, offset, n, T, 4);
     k_pcg32_gauss64<<<grid, kGenBlock, 0, as_stream(stream)>>>(a, out);
     note_launch();
     return check_launch("arv_pcg32_gaussian_f64");
 }
 
-int arv_store_probe(float *out, int64_t n, void *stream) {
-    if (n < 0 || (n & 3) || !aligned16(out)) return set_error(ARV_ERR_CONFIG, "store probe needs n % 4 == 0 and 16B alignment");
+int arv_store_probe_ex(float *out, int64_t n, int mode, void *stream) {
+    if (n < 0 || (n & 7) || !aligned(out, 32)) return set_error(ARV_ERR_CONFIG, "store probe needs n % 8 == 0 and 32B alignment");
     if (n == 0) return ARV_OK;
-    const int grid = stream_grid(n / 4, kGenBlock, kGenPerSM);
-    k_store_probe<<<grid, kGenBlock, 0, as_stream(stream)>>>(reinterpret_cast<float4 *>(out), n / 4);
+    const int G = mode == 8 ? 8 : 4;
+    const int grid = stream_grid(n / G, kGenBlock, g_ctas_per_sm);
+    uint32_t *o = reinterpret_cast<uint32_t *>(out);
+    cudaStream_t s = as_stream(stream);
+    if (mode == 8) k_store_probe<8><<<grid, kGenBlock, 0, s>>>(o, n);
+    else if (mode == 5) k_store_probe<5><<<grid, kGenBlock, 0, s>>>(o, n);
+    else k_store_probe<4><<<grid, kGenBlock, 0, s>>>(o, n);
     note_launch();
-    return check_launch("arv_store_probe");
+    return check_launch("arv_store_probe_ex");
 }
+
+int arv_store_probe(float *out, int64_t n, void *stream) { return arv_store_probe_ex(out, n, 8, stream); }
 
 }  // extern "C"
