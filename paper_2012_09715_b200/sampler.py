@@ -388,12 +388,15 @@ def sample_coupled(stream: Pcg32Stream, table, n: int) -> CoupledGaussianBatch:
 
 
 def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous [lo, hi) of ``n_total`` samples owned by ``rank`` (4-aligned)."""
+    """Contiguous [lo, hi) of ``n_total`` samples owned by ``rank``.
+
+    Boundaries are multiples of 8 samples (32 bytes), so a shard written into
+    a slice of a shared buffer keeps the 256-bit store path."""
     if world < 1 or not 0 <= rank < world:
         raise ConfigError("bad rank/world")
-    groups = (n_total + 3) // 4
+    groups = (n_total + 7) // 8
     per = groups // world
     extra = groups % world
     g_lo = rank * per + min(rank, extra)
     g_hi = g_lo + per + (1 if rank < extra else 0)
-    return min(4 * g_lo, n_total), min(4 * g_hi, n_total)
+    return min(8 * g_lo, n_total), min(8 * g_hi, n_total)
