@@ -96,6 +96,29 @@ __device__ __forceinline__ uint32_t pcg32_output(uint64_t old) {
     return __funnelshift_r(xs, xs, rot);
 }
 
+#ifndef ARV_PCG_IMADHI
+#define ARV_PCG_IMADHI 0
+#endif
+// Same output with the two right shifts of `hi` done as IMAD.HI (high word of
+// hi * 2^k) on the FMA pipe, balancing the ALU-heavy XSH-RR.  m19 = 2^19,
+// m5 = 2^5 must arrive in registers (not immediates), or ptxas folds the
+// multiply back into a shift.
+__device__ __forceinline__ uint32_t pcg32_output_fma(uint64_t old, uint32_t m19, uint32_t m5) {
+    const uint32_t lo = static_cast<uint32_t>(old);
+    const uint32_t hi = static_cast<uint32_t>(old >> 32);
+#if ARV_PCG_IMADHI >= 1
+    const uint32_t rot = __umulhi(hi, m5);  // hi >> 27
+#else
+    const uint32_t rot = hi >> 27;
+#endif
+#if ARV_PCG_IMADHI >= 2
+    const uint32_t xs = __funnelshift_r(lo, hi, 27) ^ __umulhi(hi, m19);  // hi >> 13
+#else
+    const uint32_t xs = __funnelshift_r(lo, hi, 27) ^ (hi >> 13);
+#endif
+    return __funnelshift_r(xs, xs, rot);
+}
+
 // ------------------------------------------------------ uniform mappings --
 // f32 lattice uniform u = ((w >> 9) + 0.5) 2^-23, returned in reflected form:
 //   m  = all-ones iff u >= 1/2 (i.e. the reference predicate u < 0.5 is false)

@@ -87,6 +87,7 @@ __device__ __forceinline__ void gen_loop_vec(const GenArgs &a, uint32_t *__restr
     const uint64_t z = static_cast<uint64_t>(threadIdx.x) * a.zero;  // 0, but not provably uniform
     const uint64_t inc = a.inc + z;
     const Affine st{a.stride.a + z, a.stride.c + z};
+    const uint32_t m19 = (1u << 19) + static_cast<uint32_t>(z), m5 = 32u + static_cast<uint32_t>(z);
     // Trip count once; the loop runs on a 32-bit counter and a pointer bump.
     const uint32_t iters = g0 < n_full ? static_cast<uint32_t>((n_full - g0 + T - 1) / T) : 0u;
     uint32_t *p = out + G * g0;
@@ -96,7 +97,7 @@ __device__ __forceinline__ void gen_loop_vec(const GenArgs &a, uint32_t *__restr
         uint32_t w[G];
 #pragma unroll
         for (int i = 0; i < G; ++i) {
-            w[i] = pcg32_output(s);
+            w[i] = pcg32_output_fma(s, m19, m5);
             s = i < G - 1 ? lcg_step(s, kPcgMult, inc) : lcg_step(s, st.a, st.c);
         }
         uint32_t r[G];
