@@ -24,7 +24,7 @@
 namespace arv {
 
 constexpr int kLevelBlock = 256;
-constexpr int kFinalBlock = 256;
+constexpr int kFinalBlock = 1024;
 
 struct LevelArgs {
     double a, b, c;  // GBM: mu, sigma, -; CIR: kappa, theta, sigma
@@ -126,40 +126,48 @@ __device__ __forceinline__ void chan_merge(double &n, double &mean, double &m2, 
     n = tot;
 }
 
-// Merge n_parts partials (n_parts x NK x 3) into out (NK x 3), fixed order.
-__global__ void __launch_bounds__(kFinalBlock) k_finalize(const double *__restrict__ parts, int64_t n_parts, int nk,
+// Merge n_parts partials (n_parts x NK x 3) into out (NK x 3) in a fixed
+// order: thread t folds partials t, t + B, t + 2B, ... (coalesced), then a
+// shuffle tree within each warp and a sequential fold over the warps.
+template <int NK>
+__global__ void __launch_bounds__(kFinalBlock) k_finalize(const double *__restrict__ parts, int64_t n_parts,
                                                           double *__restrict__ out) {
-    __shared__ double sh[kFinalBlock][3];
-    for (int k = 0; k < nk; ++k) {
-        const int64_t per = (n_parts + kFinalBlock - 1) / kFinalBlock;
-        const int64_t lo = threadIdx.x * per;
-        const int64_t hi = lo + per < n_parts ? lo + per : n_parts;
-        double n = 0.0, mean = 0.0, m2 = 0.0;
-        for (int64_t i = lo; i < hi; ++i) {
-            const double *p = parts + (i * nk + k) * 3;
-            chan_merge(n, mean, m2, p[0], p[1], p[2]);
+    __shared__ double sh[kFinalBlock / 32][NK][3];
+    double n[NK], mean[NK], m2[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) n[k] = mean[k] = m2[k] = 0.0;
+    for (int64_t i = threadIdx.x; i < n_parts; i += kFinalBlock) {
+        const double *p = parts + i * NK * 3;
+#pragma unroll
+        for (int k = 0; k < NK; ++k) chan_merge(n[k], mean[k], m2[k], p[3 * k], p[3 * k + 1], p[3 * k + 2]);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+            const double nb = __shfl_down_sync(0xffffffffu, n[k], o);
+            const double mb = __shfl_down_sync(0xffffffffu, mean[k], o);
+            const double qb = __shfl_down_sync(0xffffffffu, m2[k], o);
+            if ((lane & (2 * o - 1)) == 0) chan_merge(n[k], mean[k], m2[k], nb, mb, qb);
         }
-        sh[threadIdx.x][0] = n;
-        sh[threadIdx.x][1] = mean;
-        sh[threadIdx.x][2] = m2;
-        __syncthreads();
-        for (int stride = 1; stride < kFinalBlock; stride <<= 1) {
-            if ((threadIdx.x % (2 * stride)) == 0 && threadIdx.x + stride < kFinalBlock) {
-                double a0 = sh[threadIdx.x][0], a1 = sh[threadIdx.x][1], a2 = sh[threadIdx.x][2];
-                chan_merge(a0, a1, a2, sh[threadIdx.x + stride][0], sh[threadIdx.x + stride][1],
-                           sh[threadIdx.x + stride][2]);
-                sh[threadIdx.x][0] = a0;
-                sh[threadIdx.x][1] = a1;
-                sh[threadIdx.x][2] = a2;
-            }
-            __syncthreads();
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+            sh[warp][k][0] = n[k];
+            sh[warp][k][1] = mean[k];
+            sh[warp][k][2] = m2[k];
         }
-        if (threadIdx.x == 0) {
-            out[3 * k + 0] = sh[0][0];
-            out[3 * k + 1] = sh[0][1];
-            out[3 * k + 2] = sh[0][2];
-        }
-        __syncthreads();
+    }
+    __syncthreads();
+    if (threadIdx.x < NK) {
+        const int k = threadIdx.x;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int w = 0; w < kFinalBlock / 32; ++w) chan_merge(a0, a1, a2, sh[w][k][0], sh[w][k][1], sh[w][k][2]);
+        out[3 * k + 0] = a0;
+        out[3 * k + 1] = a1;
+        out[3 * k + 2] = a2;
     }
 }
 
@@ -233,12 +241,14 @@ __global__ void __launch_bounds__(kLevelBlock) k_cir_exact_level(LevelArgs A, co
                                                                  double *__restrict__ paths,
                                                                  unsigned long long *__restrict__ n_fail) {
     extern __shared__ double smd[];
+    const NcTables nct = nc_tables_init(smd, A.nu_exact);  // 4 * kNcTab doubles
     const double *tab = stacks;
     if (use_smem) {
+        double *st = smd + 4 * kNcTab;
         const int64_t total = 2 * n_knots * (DEG + 1) * K1;
-        for (int64_t k = threadIdx.x; k < total; k += blockDim.x) smd[k] = __ldg(stacks + k);
+        for (int64_t k = threadIdx.x; k < total; k += blockDim.x) st[k] = __ldg(stacks + k);
         __syncthreads();
-        tab = smd;
+        tab = st;
     }
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool valid = i < A.path_count;
@@ -258,7 +268,7 @@ __global__ void __launch_bounds__(kLevelBlock) k_cir_exact_level(LevelArgs A, co
             // mlmc.py:269-278 exact side, warm-started from the table
             const double lam_e = __dmul_rn(x_e, A.decay_over_scale);
             const double warm = ncchi2_eval1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_e);
-            const NcQuantile q = ncchi2_quantile(u, A.nu_exact, lam_e, warm);
+            const NcQuantile q = ncchi2_quantile(nct, u, A.nu_exact, lam_e, warm);
             fails += q.resid > 1e-8;
             x_e = __dmul_rn(A.scale, q.x);
         }
@@ -285,21 +295,25 @@ __global__ void __launch_bounds__(kLevelBlock) k_cir_exact_level(LevelArgs A, co
 __global__ void __launch_bounds__(256) k_ncchi2_inv(const double *__restrict__ u, const double *__restrict__ lam,
                                                     int64_t nlam, double nu, const double *__restrict__ x0,
                                                     double *__restrict__ out, double *__restrict__ resid, int64_t n) {
+    extern __shared__ double smd[];
+    const NcTables nct = nc_tables_init(smd, nu);
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const double li = nlam == 1 ? lam[0] : lam[i];
-        const NcQuantile q = ncchi2_quantile(u[i], nu, li, x0 ? x0[i] : -1.0);
+        const NcQuantile q = ncchi2_quantile(nct, u[i], nu, li, x0 ? x0[i] : -1.0);
         out[i] = q.x;
         if (resid) resid[i] = q.resid;
     }
 }
 __global__ void __launch_bounds__(256) k_ncchi2_cdf(const double *__restrict__ x, const double *__restrict__ lam,
                                                     int64_t nlam, double nu, double *__restrict__ out, int64_t n) {
+    extern __shared__ double smd[];
+    const NcTables nct = nc_tables_init(smd, nu);
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const double li = nlam == 1 ? lam[0] : lam[i];
         const double xi = x[i];
-        out[i] = xi <= 0.0 ? 0.0 : ncchi2_cdf_minus(xi, nu, li, 0.0, 1.0).resid;
+        out[i] = xi <= 0.0 ? 0.0 : ncchi2_cdf_minus(nct, xi, li, 0.0, 1.0).resid;
     }
 }
 
@@ -338,7 +352,7 @@ static int fill_common(const arv_level_spec *sp, LevelArgs &A) {
 static int64_t n_blocks_for(int64_t count) { return (count + kLevelBlock - 1) / kLevelBlock; }
 
 static int run_finalize(double *parts, int64_t nb, double *stats, cudaStream_t s, const char *what) {
-    k_finalize<<<1, kFinalBlock, 0, s>>>(parts, nb, ARV_NKIND, stats);
+    k_finalize<ARV_NKIND><<<1, kFinalBlock, 0, s>>>(parts, nb, stats);
     note_launch();
     return check_launch(what);
 }
@@ -425,8 +439,8 @@ int arv_mlmc_cir_exact_level(const arv_level_spec *spec, const double *stacks, i
         return set_error(ARV_ERR_CONFIG, "workspace too small");
     double *parts = static_cast<double *>(workspace);
     const size_t bytes = sizeof(double) * 2 * n_knots * (degree + 1) * K1;
-    const int use_smem = bytes <= 160 * 1024;
-    const size_t smem = use_smem ? bytes : 0;
+    const int use_smem = bytes <= 128 * 1024;
+    const size_t smem = sizeof(double) * 4 * kNcTab + (use_smem ? bytes : 0);
     cudaStream_t s = as_stream(stream);
     unsigned long long *nf = reinterpret_cast<unsigned long long *>(n_fail);
 #define ARV_CASE(D)                                                                                          \
@@ -454,7 +468,8 @@ int arv_ncchi2_inv_cdf(const double *u, const double *lam, int64_t nlam, double 
     if (!(nu > 0)) return set_error(ARV_ERR_DOMAIN, "degrees of freedom must be > 0");
     if (nlam != 1 && nlam != n) return set_error(ARV_ERR_CONFIG, "per-element lambda must match the shape of u");
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
-    k_ncchi2_inv<<<stream_grid(n, 256, 8), 256, 0, as_stream(stream)>>>(u, lam, nlam, nu, x0, out, resid, n);
+    const size_t smem = sizeof(double) * 4 * kNcTab;
+    k_ncchi2_inv<<<stream_grid(n, 256, 8), 256, smem, as_stream(stream)>>>(u, lam, nlam, nu, x0, out, resid, n);
     note_launch();
     return check_launch("arv_ncchi2_inv_cdf");
 }
@@ -463,7 +478,8 @@ int arv_ncchi2_cdf(const double *x, const double *lam, int64_t nlam, double nu, 
     if (!(nu > 0)) return set_error(ARV_ERR_DOMAIN, "degrees of freedom must be > 0");
     if (nlam != 1 && nlam != n) return set_error(ARV_ERR_CONFIG, "per-element lambda must match the shape of x");
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
-    k_ncchi2_cdf<<<stream_grid(n, 256, 8), 256, 0, as_stream(stream)>>>(x, lam, nlam, nu, out, n);
+    const size_t smem = sizeof(double) * 4 * kNcTab;
+    k_ncchi2_cdf<<<stream_grid(n, 256, 8), 256, smem, as_stream(stream)>>>(x, lam, nlam, nu, out, n);
     note_launch();
     return check_launch("arv_ncchi2_cdf");
 }

@@ -19,11 +19,50 @@
 // through the recurrence, so tails keep their relative accuracy.  Poisson
 // weights are renormalised by their computed sum, cancelling the common
 // rounding of exp/lgamma in the mode weight.
+//
+// Speed: every per-term division of the recurrences uses a per-CTA shared
+// table -- 1/j, 1/(nu/2 + j), lgamma(j + 1), lgamma(nu/2 + j + 1) for
+// j < kNcTab -- so the inner loops are multiply/add only; indices past the
+// table fall back to direct division / lgamma.
 #pragma once
 
 #include "arv_common.cuh"
 
 namespace arv {
+
+constexpr int kNcTab = 1024;
+
+struct NcTables {
+    const double *inv_j;   // 1 / j            (inv_j[0] unused)
+    const double *inv_aj;  // 1 / (a0 + j)
+    const double *lg_j;    // lgamma(j + 1)
+    const double *lg_aj;   // lgamma(a0 + j + 1)
+    double a0;
+
+    __device__ __forceinline__ double rj(long long j) const { return j < kNcTab ? inv_j[j] : 1.0 / j; }
+    __device__ __forceinline__ double raj(long long j) const {
+        return j < kNcTab ? inv_aj[j] : 1.0 / (a0 + static_cast<double>(j));
+    }
+    __device__ __forceinline__ double lgj(long long j) const {
+        return j < kNcTab ? lg_j[j] : lgamma(static_cast<double>(j) + 1.0);
+    }
+    __device__ __forceinline__ double lgaj(long long j) const {
+        return j < kNcTab ? lg_aj[j] : lgamma(a0 + static_cast<double>(j) + 1.0);
+    }
+};
+
+// Fill the tables in shared memory (4 * kNcTab doubles) for a0 = nu / 2.
+__device__ inline NcTables nc_tables_init(double *sm, double nu) {
+    const double a0 = 0.5 * nu;
+    for (int j = threadIdx.x; j < kNcTab; j += blockDim.x) {
+        sm[j] = j ? 1.0 / j : 0.0;
+        sm[kNcTab + j] = 1.0 / (a0 + j);
+        sm[2 * kNcTab + j] = lgamma(static_cast<double>(j) + 1.0);
+        sm[3 * kNcTab + j] = lgamma(a0 + static_cast<double>(j) + 1.0);
+    }
+    __syncthreads();
+    return {sm, sm + kNcTab, sm + 2 * kNcTab, sm + 3 * kNcTab, a0};
+}
 
 struct GammaPQ {
     double small;  // P if lower, else Q
@@ -31,17 +70,17 @@ struct GammaPQ {
     double G;      // y^a e^-y / Gamma(a+1)
 };
 
-// Regularized incomplete gamma at (a, y), a > 0, y > 0.
-__device__ inline GammaPQ gamma_pq(double a, double y) {
-    const double lg = lgamma(a + 1.0);
-    const double G = exp(a * log(y) - y - lg);
+// Regularized incomplete gamma at (a, y) = (a0 + k, y), y > 0.
+__device__ inline GammaPQ gamma_pq(const NcTables &t, long long k, double y, double log_y) {
+    const double a = t.a0 + static_cast<double>(k);
+    const double G = exp(a * log_y - y - t.lgaj(k));
     GammaPQ r;
     r.G = G;
     if (y < a + 1.0) {
-        // P = G * sum_{n>=0} y^n / ((a+1)...(a+n))
+        // P = G * sum_{n>=0} y^n / ((a+1)...(a+n)),  1/(a+n) = 1/(a0+k+n)
         double sum = 1.0, term = 1.0;
-        for (int n = 1; n < 2000; ++n) {
-            term *= y / (a + n);
+        for (long long n = 1; n < 4000; ++n) {
+            term *= y * t.raj(k + n);
             sum += term;
             if (term < sum * 1e-17) break;
         }
@@ -78,35 +117,36 @@ struct NcCdf {
 };
 
 // F(x) - u and f(x) for x > 0.  `one_minus_u` is exact for u >= 1/2.
-__device__ inline NcCdf ncchi2_cdf_minus(double x, double nu, double lam, double u, double one_minus_u) {
+__device__ inline NcCdf ncchi2_cdf_minus(const NcTables &t, double x, double lam, double u, double one_minus_u) {
     const double y = 0.5 * x;
-    const double a0 = 0.5 * nu;
+    const double a0 = t.a0;
     const double h = 0.5 * lam;
     const double kd = floor(h);
     const long long k = static_cast<long long>(kd);
-    const double pk = h > 0.0 ? exp(-h + kd * log(h) - lgamma(kd + 1.0)) : 1.0;
+    const double pk = h > 0.0 ? exp(-h + kd * log(h) - t.lgj(k)) : 1.0;
+    const double inv_y = 1.0 / y;
+    const double inv_h = h > 0.0 ? 1.0 / h : 0.0;
 
-    const GammaPQ g = gamma_pq(a0 + kd, y);
+    const GammaPQ g = gamma_pq(t, k, y, log(y));
     const bool lower = g.lower;
     // Mode term.  Carried side S_j: P_j (lower) or Q_j (upper).
     double wsum = pk;
     double acc = pk * g.small;
     // density: 1/2 pk G(a0 + k - 1) = 1/2 pk G_k (a0 + k) / y
-    double dens = pk * g.G * (a0 + kd) / y;
+    double dens = pk * g.G * (a0 + kd) * inv_y;
 
     // forward j = k+1, k+2, ...
     {
         double p = pk, S = g.small, G = g.G;
         for (long long j = k + 1; j < k + 100000; ++j) {
-            const double jd = static_cast<double>(j);
-            p *= h / jd;
+            p *= h * t.rj(j);
             // S_j from S_{j-1}: P decreases by G_{j-1}, Q increases by it
             S = lower ? fmax(S - G, 0.0) : S + G;
             dens += p * G;  // G_{j-1} = G(a0 + j - 1)
-            G *= y / (a0 + jd);
+            G *= y * t.raj(j);
             wsum += p;
             acc += p * S;
-            if (p < 1e-18 && jd > h) break;
+            if (p < 1e-18 && static_cast<double>(j) > h) break;
         }
     }
     // backward j = k-1, ..., 0
@@ -114,12 +154,12 @@ __device__ inline NcCdf ncchi2_cdf_minus(double x, double nu, double lam, double
         double p = pk, S = g.small, G = g.G;
         for (long long j = k - 1; j >= 0; --j) {
             const double jd = static_cast<double>(j);
-            p *= (jd + 1.0) / h;
-            G *= (a0 + jd + 1.0) / y;  // G_j = G_{j+1} (a0 + j + 1) / y
+            p *= (jd + 1.0) * inv_h;
+            G *= (a0 + jd + 1.0) * inv_y;  // G_j = G_{j+1} (a0 + j + 1) / y
             S = lower ? S + G : fmax(S - G, 0.0);
             wsum += p;
             acc += p * S;
-            dens += p * G * (a0 + jd) / y;  // G_{j-1}
+            dens += p * G * (a0 + jd) * inv_y;  // G_{j-1}
             if (p < 1e-18) break;
         }
     }
@@ -136,14 +176,14 @@ struct NcQuantile {
 };
 
 // exact_dist.py:381-461 contract, per element, warm start x0 (<= 0: mean).
-__device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, double x0) {
+__device__ inline NcQuantile ncchi2_quantile(const NcTables &t, double u, double nu, double lam, double x0) {
     const double one_minus_u = 1.0 - u;
     double hi = lam + nu + 20.0 * sqrt(2.0 * (lam + nu)) + 100.0;
     double lo = 0.0;
     const double tol_f = fmin(1e-9, fmax(1e-13, 1e-4 * fmin(u, one_minus_u)));
     double x = x0 > 0.0 ? x0 : lam + nu;
     x = fmin(fmax(x, 1e-8), hi);
-    NcCdf c = ncchi2_cdf_minus(x, nu, lam, u, one_minus_u);
+    NcCdf c = ncchi2_cdf_minus(t, x, lam, u, one_minus_u);
     for (int it = 0; it < 80; ++it) {
         if (fabs(c.resid) <= tol_f) break;
         if (c.resid > 0.0) hi = x;
@@ -151,7 +191,7 @@ __device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, do
         double xn = x - c.resid / c.pdf;
         if (!isfinite(xn) || xn <= lo || xn >= hi) xn = 0.5 * (lo + hi);
         x = xn;
-        c = ncchi2_cdf_minus(x, nu, lam, u, one_minus_u);
+        c = ncchi2_cdf_minus(t, x, lam, u, one_minus_u);
         if (hi - lo < 1e-15 * hi) break;
     }
     return {x, fabs(c.resid)};
