@@ -107,6 +107,21 @@ ARV_API int arv_pcg32_gaussian_f64(uint64_t seed, uint64_t stream_id, uint64_t o
                            void *stream);
 ARV_API int arv_pcg32_gaussian_f32(uint64_t seed, uint64_t stream_id, uint64_t offset, float *out, int64_t n,
                            void *stream);
+/* ---- Philox-4x64-10 replay of the reference's UniformStream --------------
+ * sampler.py:26-66: key [seed, stream_id], word n = Philox(ctr=[n/4+1,...],
+ * key)[n % 4] -- bit-exact with numpy.random.Philox.  `counter` = index of
+ * the first 64-bit word (UniformStream.counter). */
+ARV_API int arv_philox_words(uint64_t seed, uint64_t stream_id, uint64_t counter, uint64_t *out, int64_t n,
+                             void *stream);
+/* Fused Philox -> evaluator, f64 out (the reference's default evaluate()):
+ * kind 0 = uniforms ((w >> 11) + 0.5) 2^-53 (sampler.py:59-62);
+ * kind 1 = constant_eval, table = values f64[table_cols];
+ * kind 2 = dyadic_eval, table = coeffs f64[degree+1][table_cols];
+ * kind 3 = AS241 gaussian_inv_cdf (table unused). */
+ARV_API int arv_philox_eval_f64(uint64_t seed, uint64_t stream_id, uint64_t counter, int kind,
+                                const double *table, int degree, int64_t table_cols, double *out, int64_t n,
+                                void *stream);
+
 /* Write-only bandwidth probes (streaming stores of a constant): the store
  * roof.  mode 4 = st.global.cs.v4, 8 = st.global.cs.v8 (256-bit), 5 =
  * st.global.v4; arv_store_probe = mode 8.  n % 8 == 0, out 32-byte aligned. */
@@ -121,9 +136,12 @@ ARV_API int arv_store_probe_ex(float *out, int64_t n, int mode, void *stream);
 ARV_API int arv_set_tuning(int key, int value);
 
 /* ---- nested MLMC level kernels ------------------------------------------
- * Path p of a level uses PCG32 outputs k*n_paths_total + p (fine step k) of
- * stream (seed, stream_id): the reference's addressing (mlmc.py:200-202)
- * with Philox words replaced by PCG32 outputs; f64 uniform (w + 0.5) 2^-32.
+ * Path p of a level uses word k*n_paths_total + p (fine step k) of stream
+ * (seed, stream_id): the reference's addressing (mlmc.py:200-202).  With
+ * rng = ARV_RNG_PHILOX the words are the reference's own Philox-4x64-10
+ * UniformStream words and u = ((w >> 11) + 0.5) 2^-53 (path-by-path replay
+ * of the reference); with ARV_RNG_PCG32 they are PCG32 outputs and
+ * u = (w + 0.5) 2^-32.
  * A call simulates global paths [path_lo, path_lo + path_count).
  *
  * stats (device f64[3 * ARV_NKIND]) receives per kind (count, mean, M2) of
@@ -142,6 +160,8 @@ ARV_API int arv_set_tuning(int key, int value);
 #define ARV_SCHEME_CIR_EXACT 2
 #define ARV_SCHEME_CIR_EULER_TRUNCATED 3
 #define ARV_SCHEME_CIR_MILSTEIN_TRUNCATED 4
+#define ARV_RNG_PCG32 0
+#define ARV_RNG_PHILOX 1
 #define ARV_PAYOFF_IDENTITY 0
 #define ARV_PAYOFF_CALL 1
 
@@ -153,6 +173,7 @@ typedef struct {
     double strike;
     uint64_t seed, stream_id;
     int64_t n_paths_total, path_lo, path_count;
+    int rng; /* ARV_RNG_PCG32 or ARV_RNG_PHILOX */
 } arv_level_spec;
 
 ARV_API int64_t arv_mlmc_workspace_bytes(int64_t path_count);

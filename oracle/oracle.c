@@ -509,3 +509,66 @@ EXPORT void orc_cir_euler_paths(double kappa, double theta, double sigma, double
     }
 #undef CIR_EM
 }
+
+/* ------------------------------------------------------------------------ */
+/* Philox-4x64-10 (Salmon et al. 2011; numpy.random.Philox), the reference's */
+/* uniform source: UniformStream (sampler.py:26-66) keys it with            */
+/* [seed, stream_id]; word n is Philox(ctr=[n/4 + 1, 0, 0, 0], key)[n % 4]   */
+/* (numpy pre-increments the 256-bit counter), u = ((w >> 11) + 0.5) 2^-53.  */
+/* ------------------------------------------------------------------------ */
+static const uint64_t PH_M0 = 0xD2E7470EE14C6C93ULL, PH_M1 = 0xCA5A826395121157ULL;
+static const uint64_t PH_W0 = 0x9E3779B97F4A7C15ULL, PH_W1 = 0xBB67AE8584CAA73BULL;
+
+static inline void philox4x64_10(const uint64_t ctr[4], uint64_t k0, uint64_t k1, uint64_t out[4]) {
+    uint64_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += PH_W0;
+            k1 += PH_W1;
+        }
+        __uint128_t p0 = (__uint128_t)PH_M0 * c0, p1 = (__uint128_t)PH_M1 * c2;
+        uint64_t hi0 = (uint64_t)(p0 >> 64), lo0 = (uint64_t)p0;
+        uint64_t hi1 = (uint64_t)(p1 >> 64), lo1 = (uint64_t)p1;
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+    }
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+    out[3] = c3;
+}
+
+/* 64-bit words [start, start+n) of UniformStream(seed, stream_id). */
+EXPORT void orc_philox_words(uint64_t seed, uint64_t sid, uint64_t start, int64_t n, uint64_t *out) {
+    uint64_t blk[4];
+    uint64_t cur = UINT64_MAX;
+    for (int64_t i = 0; i < n; ++i) {
+        uint64_t w = start + (uint64_t)i;
+        uint64_t b = w >> 2;
+        if (b != cur) {
+            /* counter = b + 1 as a 256-bit integer (carry into word 1) */
+            uint64_t ctr[4] = {b + 1, b + 1 == 0 ? 1u : 0u, 0, 0};
+            philox4x64_10(ctr, seed, sid, blk);
+            cur = b;
+        }
+        out[i] = blk[w & 3];
+    }
+}
+
+/* UniformStream.uniforms (sampler.py:59-62) */
+EXPORT void orc_philox_uniforms(uint64_t seed, uint64_t sid, uint64_t start, int64_t n, double *out) {
+    uint64_t blk[4];
+    uint64_t cur = UINT64_MAX;
+    for (int64_t i = 0; i < n; ++i) {
+        uint64_t w = start + (uint64_t)i;
+        uint64_t b = w >> 2;
+        if (b != cur) {
+            uint64_t ctr[4] = {b + 1, b + 1 == 0 ? 1u : 0u, 0, 0};
+            philox4x64_10(ctr, seed, sid, blk);
+            cur = b;
+        }
+        out[i] = ((double)(blk[w & 3] >> 11) + 0.5) * 0x1p-53;
+    }
+}

@@ -76,6 +76,24 @@ _sig("orc_cir_euler_paths", _dbl, _dbl, _dbl, _dbl, _dbl, _int, _int, _int, _dbl
      _u64, _u64, _i64, _i64, _i64, _p, _p, _p, _p)
 
 
+_sig("orc_philox_words", _u64, _u64, _u64, _i64, _p)
+_sig("orc_philox_uniforms", _u64, _u64, _u64, _i64, _p)
+
+
+def philox_words(seed: int, sid: int, counter: int, n: int) -> np.ndarray:
+    """UniformStream(seed, sid, counter).raw_words(n) (sampler.py:48-57)."""
+    out = np.empty(n, dtype=np.uint64)
+    lib.orc_philox_words(seed, sid, counter, n, out.ctypes.data_as(C.c_void_p))
+    return out
+
+
+def philox_uniforms(seed: int, sid: int, counter: int, n: int) -> np.ndarray:
+    """UniformStream(seed, sid, counter).uniforms(n) (sampler.py:59-62)."""
+    out = np.empty(n, dtype=np.float64)
+    lib.orc_philox_uniforms(seed, sid, counter, n, out.ctypes.data_as(C.c_void_p))
+    return out
+
+
 def _ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 

@@ -20,7 +20,7 @@ from .mlmc import (
     level_stream, optimal_allocation, optimal_allocation_nested, simulate, speedup_report,
 )
 from .sampler import (
-    CoupledGaussianBatch, Pcg32Stream, dyadic_index, eval_constant, eval_dyadic, eval_ncchi2,
+    CoupledGaussianBatch, Pcg32Stream, PhiloxStream, dyadic_index, eval_constant, eval_dyadic, eval_ncchi2,
     eval_subdyadic, evaluate, gaussian_inv_cdf, sample_coupled, shard_range,
 )
 from .tables import ConstantTable, DyadicPolyTable, NcChi2Table, SubDyadicTable, load_table, shipped_names
@@ -31,7 +31,7 @@ __all__ = [
     "Allocation", "CirParams", "GbmParams", "LevelSpec", "LevelStats", "estimate_level",
     "estimate_level_suite", "level_stream", "optimal_allocation", "optimal_allocation_nested",
     "simulate", "speedup_report",
-    "CoupledGaussianBatch", "Pcg32Stream", "dyadic_index", "eval_constant", "eval_dyadic", "eval_ncchi2",
+    "CoupledGaussianBatch", "Pcg32Stream", "PhiloxStream", "dyadic_index", "eval_constant", "eval_dyadic", "eval_ncchi2",
     "eval_subdyadic", "evaluate", "gaussian_inv_cdf", "sample_coupled", "shard_range",
     "ConstantTable", "DyadicPolyTable", "NcChi2Table", "SubDyadicTable", "load_table", "shipped_names",
     "backend_name", "get_kernels",

@@ -26,11 +26,14 @@ class LevelSpec(C.Structure):
         ("strike", _dbl),
         ("seed", _u64), ("stream_id", _u64),
         ("n_paths_total", _i64), ("path_lo", _i64), ("path_count", _i64),
+        ("rng", _int),
     ]
 
 
 SCHEME_EM, SCHEME_MILSTEIN, SCHEME_CIR_EXACT, SCHEME_CIR_EULER_TRUNCATED, SCHEME_CIR_MILSTEIN_TRUNCATED = range(5)
 PAYOFF_IDENTITY, PAYOFF_CALL = 0, 1
+RNG_PCG32, RNG_PHILOX = 0, 1
+PHILOX_UNIFORM, PHILOX_CONSTANT, PHILOX_DYADIC, PHILOX_GAUSSIAN = range(4)
 
 _SIGNATURES = {
     "arv_abi_version": ([], _int),
@@ -51,6 +54,8 @@ _SIGNATURES = {
     "arv_pcg32_subdyadic_f32": ([_u64, _u64, _u64, _p, _int, _int, _int, _p, _i64, _p], _int),
     "arv_pcg32_gaussian_f64": ([_u64, _u64, _u64, _p, _i64, _p], _int),
     "arv_pcg32_gaussian_f32": ([_u64, _u64, _u64, _p, _i64, _p], _int),
+    "arv_philox_words": ([_u64, _u64, _u64, _p, _i64, _p], _int),
+    "arv_philox_eval_f64": ([_u64, _u64, _u64, _int, _p, _int, _i64, _p, _i64, _p], _int),
     "arv_store_probe": ([_p, _i64, _p], _int),
     "arv_store_probe_ex": ([_p, _i64, _int, _p], _int),
     "arv_set_tuning": ([_int, _int], _int),

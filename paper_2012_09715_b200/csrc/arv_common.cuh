@@ -119,6 +119,45 @@ __device__ __forceinline__ uint32_t pcg32_output_fma(uint64_t old, uint32_t m19,
     return __funnelshift_r(xs, xs, rot);
 }
 
+// ------------------------------------------------------- Philox-4x64-10 --
+// The reference's own uniform source (numpy.random.Philox behind
+// UniformStream, sampler.py:26-66): key = [seed, stream_id], word n of the
+// stream = Philox(ctr = [n/4 + 1, carry, 0, 0], key)[n % 4] (numpy
+// pre-increments the 256-bit counter), u = ((w >> 11) + 0.5) 2^-53.
+struct Philox4 {
+    uint64_t w[4];
+};
+__device__ __forceinline__ Philox4 philox4x64_10(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3, uint64_t k0,
+                                                 uint64_t k1) {
+    constexpr uint64_t M0 = 0xD2E7470EE14C6C93ULL, M1 = 0xCA5A826395121157ULL;
+    constexpr uint64_t W0 = 0x9E3779B97F4A7C15ULL, W1 = 0xBB67AE8584CAA73BULL;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += W0;
+            k1 += W1;
+        }
+        const uint64_t hi0 = __umul64hi(M0, c0), lo0 = M0 * c0;
+        const uint64_t hi1 = __umul64hi(M1, c2), lo1 = M1 * c2;
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+    }
+    return {{c0, c1, c2, c3}};
+}
+// Word `n` of UniformStream(seed, stream_id).
+__device__ __forceinline__ uint64_t philox_word(uint64_t n, uint64_t seed, uint64_t sid) {
+    const uint64_t b = (n >> 2) + 1;
+    const Philox4 r = philox4x64_10(b, b == 0 ? 1u : 0u, 0, 0, seed, sid);
+    const int lane = static_cast<int>(n & 3);
+    return lane == 0 ? r.w[0] : lane == 1 ? r.w[1] : lane == 2 ? r.w[2] : r.w[3];
+}
+// sampler.py:62: ((w >> 11) + 0.5) * 2^-53, exact.
+__device__ __forceinline__ double u64_to_f64(uint64_t w) {
+    return __dmul_rn(__dadd_rn(static_cast<double>(w >> 11), 0.5), 0x1p-53);
+}
+
 // ------------------------------------------------------ uniform mappings --
 // f32 lattice uniform u = ((w >> 9) + 0.5) 2^-23, returned in reflected form:
 //   m  = all-ones iff u >= 1/2 (i.e. the reference predicate u < 0.5 is false)

@@ -37,6 +37,38 @@ struct LevelArgs {
     int64_t path_lo, path_count;
     // CIR exact
     double nu_exact, nu_table, scale, decay_over_scale;
+    // uniform source
+    int rng;             // ARV_RNG_PCG32 / ARV_RNG_PHILOX
+    uint64_t seed, sid;  // Philox key
+    uint64_t n_paths_total;
+};
+
+// Per-path uniform source: word k * n_paths_total + p for fine step k.
+struct PathRng {
+    uint64_t s;       // PCG32 state / Philox word index
+    Affine step;
+    uint64_t n_paths, seed, sid;
+    int philox;
+    __device__ __forceinline__ PathRng(const LevelArgs &A, uint64_t p)
+        : step(A.step), n_paths(A.n_paths_total), seed(A.seed), sid(A.sid), philox(A.rng == ARV_RNG_PHILOX) {
+        if (philox) {
+            s = p;
+        } else {
+            const Affine jp = lcg_jump(p, A.inc);
+            s = jp.a * A.s0 + jp.c;
+        }
+    }
+    __device__ __forceinline__ double next() {
+        double u;
+        if (philox) {
+            u = u64_to_f64(philox_word(s, seed, sid));  // sampler.py:62
+            s += n_paths;
+        } else {
+            u = u32_to_f64(pcg32_output(s));
+            s = step.a * s + step.c;
+        }
+        return u;
+    }
 };
 
 __device__ __forceinline__ double payoff_fn(double x, int payoff, double strike) {
@@ -188,8 +220,7 @@ __global__ void __launch_bounds__(kLevelBlock) k_gaussian_level(LevelArgs A, con
     double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (valid) {
         const uint64_t p = static_cast<uint64_t>(A.path_lo + i);
-        const Affine jp = lcg_jump(p, A.inc);
-        uint64_t s = jp.a * A.s0 + jp.c;
+        PathRng rng(A, p);
         const double x0 = A.x0, dt_f = A.dt_f, dt_c = A.dt_c, sq_f = A.sq_f;
         double xf_e = x0, xc_e = x0, xf_a = x0, xc_a = x0;
         auto step = [&](double x, double dw, double dt) -> double {
@@ -197,10 +228,8 @@ __global__ void __launch_bounds__(kLevelBlock) k_gaussian_level(LevelArgs A, con
             else return cir_step<MIL>(x, dw, dt, A.a, A.b, A.c);
         };
         for (int64_t pair = 0; pair < A.n_f / 2; ++pair) {
-            const double u1 = u32_to_f64(pcg32_output(s));
-            s = A.step.a * s + A.step.c;
-            const double u2 = u32_to_f64(pcg32_output(s));
-            s = A.step.a * s + A.step.c;
+            const double u1 = rng.next();
+            const double u2 = rng.next();
             const double z1 = as241_f64(u1), z2 = as241_f64(u2);
             xf_e = step(step(xf_e, __dmul_rn(sq_f, z1), dt_f), __dmul_rn(sq_f, z2), dt_f);
             xc_e = step(xc_e, __dmul_rn(sq_f, __dadd_rn(z1, z2)), dt_c);
@@ -209,7 +238,7 @@ __global__ void __launch_bounds__(kLevelBlock) k_gaussian_level(LevelArgs A, con
             xc_a = step(xc_a, __dmul_rn(sq_f, __dadd_rn(w1, w2)), dt_c);
         }
         if (A.n_f & 1) {
-            const double u1 = u32_to_f64(pcg32_output(s));
+            const double u1 = rng.next();
             xf_e = step(xf_e, __dmul_rn(sq_f, as241_f64(u1)), dt_f);
             xf_a = step(xf_a, __dmul_rn(sq_f, dyadic_eval1<DEG>(smd, K1, u1)), dt_f);
         }
@@ -255,13 +284,11 @@ __global__ void __launch_bounds__(kLevelBlock) k_cir_exact_level(LevelArgs A, co
     double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (valid) {
         const uint64_t p = static_cast<uint64_t>(A.path_lo + i);
-        const Affine jp = lcg_jump(p, A.inc);
-        uint64_t s = jp.a * A.s0 + jp.c;
+        PathRng rng(A, p);
         double x_e = A.x0, x_a = A.x0;
         unsigned fails = 0;
         for (int64_t k = 0; k < A.n_f; ++k) {
-            const double u = u32_to_f64(pcg32_output(s));
-            s = A.step.a * s + A.step.c;
+            const double u = rng.next();
             // mlmc.py:264-268 approximate side (state clamped before lambda)
             const double lam_a = __dmul_rn(fmax(x_a, 0.0), A.decay_over_scale);
             x_a = __dmul_rn(A.scale, ncchi2_eval1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_a));
@@ -343,6 +370,11 @@ static int fill_common(const arv_level_spec *sp, LevelArgs &A) {
     A.s0 = st.state;
     A.inc = st.inc;
     A.step = lcg_jump(static_cast<uint64_t>(sp->n_paths_total), st.inc);
+    if (sp->rng != ARV_RNG_PCG32 && sp->rng != ARV_RNG_PHILOX) return set_error(ARV_ERR_CONFIG, "unknown rng %d", sp->rng);
+    A.rng = sp->rng;
+    A.seed = sp->seed;
+    A.sid = sp->stream_id;
+    A.n_paths_total = static_cast<uint64_t>(sp->n_paths_total);
     A.path_lo = sp->path_lo;
     A.path_count = sp->path_count;
     A.nu_exact = A.nu_table = A.scale = A.decay_over_scale = 0.0;

@@ -26,7 +26,7 @@ import torch
 from . import _device as dev
 from . import _native as nat
 from .errors import ConfigError, NumericalError
-from .sampler import Pcg32Stream
+from .sampler import PhiloxStream, Pcg32Stream
 from .tables import ConstantTable, DyadicPolyTable, NcChi2Table, SubDyadicTable, load_table
 
 SCHEMES = ("euler_maruyama", "milstein", "cir_exact", "cir_euler_truncated", "cir_milstein_truncated")
@@ -161,9 +161,19 @@ class PathBatch:
     draws_per_path: int
 
 
-def level_stream(seed: int, level: int, batch_index: int = 0) -> Pcg32Stream:
-    """Deterministic disjoint stream for (level, batch) workers (mlmc.py:414-416)."""
-    return Pcg32Stream(seed, stream_id=(level << 32) | batch_index)
+def level_stream(seed: int, level: int, batch_index: int = 0, generator: str = "pcg32"):
+    """Deterministic disjoint stream for (level, batch) workers (mlmc.py:414-416).
+
+    ``generator="philox"`` gives the reference's own UniformStream words
+    (Philox-4x64-10), so device paths replay the reference path by path;
+    the default is PCG32 (BASELINE.json).
+    """
+    sid = (level << 32) | batch_index
+    if generator == "philox":
+        return PhiloxStream(seed, stream_id=sid)
+    if generator != "pcg32":
+        raise ConfigError(f"unknown generator {generator!r}")
+    return Pcg32Stream(seed, stream_id=sid)
 
 
 # ---------------------------------------------------------------------------
@@ -208,6 +218,7 @@ def _native_spec(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, path_lo: in
     s.strike = spec.strike
     s.seed, s.stream_id = int(stream.seed), int(stream.stream_id)
     s.n_paths_total, s.path_lo, s.path_count = n_paths, path_lo, path_count
+    s.rng = nat.RNG_PHILOX if isinstance(stream, PhiloxStream) else nat.RNG_PCG32
     return s
 
 

@@ -332,6 +332,76 @@ class Pcg32Stream:
         return out
 
 
+@dataclass
+class PhiloxStream:
+    """The reference's UniformStream (sampler.py:26-66), replayed on the device.
+
+    Philox-4x64-10 keyed with (seed, stream_id); ``counter`` indexes 64-bit
+    words; ``uniforms`` are ((w >> 11) + 0.5) 2^-53 in f64 -- bit-exact with
+    ``approxrv.sampler.UniformStream(seed, stream_id, counter)``, so device
+    results can be replayed path by path against the reference.
+    """
+
+    seed: int
+    stream_id: int = 0
+    counter: int = 0
+
+    def __post_init__(self):
+        if not 0 <= int(self.seed) <= _MAX64 or not 0 <= int(self.stream_id) <= _MAX64:
+            raise ConfigError("seed and stream_id must fit in 64 bits")
+
+    def _take(self, n: int) -> int:
+        if n < 0:
+            raise ConfigError("cannot draw a negative number of words")
+        start = self.counter
+        self.counter = start + n
+        return start
+
+    def child(self, stream_id: int) -> "PhiloxStream":
+        return PhiloxStream(self.seed, stream_id)
+
+    def raw_words(self, n: int, device=None) -> torch.Tensor:
+        """The next n raw 64-bit words (uint64 device tensor), advancing the counter."""
+        start = self._take(n)
+        o = torch.empty(n, dtype=torch.uint64, device=device or dev.require_cuda())
+        call("arv_philox_words", self.seed, self.stream_id, start, o.data_ptr(), n, dev.stream_handle(o.device))
+        return o
+
+    def _eval(self, kind, n, table=None, degree=0, cols=0, out=None, device=None):
+        start = self._take(n)
+        o = out if out is not None else torch.empty(n, dtype=torch.float64, device=device or dev.require_cuda())
+        if not (dev.is_device_tensor(o) and o.dtype == torch.float64 and o.is_contiguous() and o.numel() == n):
+            raise ConfigError(f"out must be a contiguous CUDA float64 tensor of {n} elements")
+        tp = table.data_ptr() if table is not None else None
+        call("arv_philox_eval_f64", self.seed, self.stream_id, start, kind, tp, degree, cols, o.data_ptr(), n,
+             dev.stream_handle(o.device))
+        return o
+
+    def uniforms(self, n: int, out=None, device=None) -> torch.Tensor:
+        """n doubles in (0, 1) (sampler.py:59-62)."""
+        return self._eval(_PH_UNIFORM, n, out=out, device=device)
+
+    def sample(self, table, n: int, out=None, device=None) -> torch.Tensor:
+        """Fused ``evaluate(table, self.uniforms(n))`` in f64 (the reference default).
+
+        ``table`` is a ConstantTable, DyadicPolyTable (decay 1/2) or ``"exact"`` (AS241).
+        """
+        device = device or dev.require_cuda()
+        if _is(table, "ConstantTable", ConstantTable):
+            v = dev.table_on_device(table.values, torch.float64, device)
+            return self._eval(_PH_CONSTANT, n, v, 0, v.numel(), out, device)
+        if _is(table, "DyadicPolyTable", DyadicPolyTable):
+            if getattr(table, "decay", 0.5) != 0.5:
+                raise ConfigError("the fused path requires decay rate 1/2")
+            c = dev.table_on_device(table.coeffs, torch.float64, device)
+            return self._eval(_PH_DYADIC, n, c, c.shape[0] - 1, c.shape[1], out, device)
+        if isinstance(table, str) and table == "exact":
+            return self._eval(_PH_GAUSSIAN, n, out=out, device=device)
+        raise ConfigError(f"cannot sample from object of type {type(table).__name__}")
+
+
+_PH_UNIFORM, _PH_CONSTANT, _PH_DYADIC, _PH_GAUSSIAN = range(4)
+
 _SIDE: dict = {}
 _BUFS: dict = {}
 

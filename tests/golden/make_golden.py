@@ -148,6 +148,31 @@ def main() -> None:
     h["gbm_cases"] = [list(c) for c in cases]
     h["gbm_n_paths"] = n_paths
 
+    # ------------------------------- Philox replay (the reference's own streams)
+    # UniformStream itself (no substitution): uniforms, evaluate() and the GBM
+    # pilot exactly as the reference runs them with level_stream(seed, level).
+    from approxrv import sampler as ref_sampler
+
+    g["philox_uniforms_5_3_c13"] = ref_sampler.UniformStream(5, (3 << 32) | 1, counter=13).uniforms(4099)
+    g["philox_words_42_7"] = ref_sampler.UniformStream(42, 7).raw_words(64)
+    uu = ref_sampler.UniformStream(42, 9).uniforms(8192)
+    g["philox_eval_dyadic_lin"] = ref_sampler.evaluate(lin, uu)
+    g["philox_eval_const"] = ref_sampler.evaluate(ref_const_table(), uu)
+    g["philox_eval_exact"] = exact_dist.gaussian_inv_cdf(uu)
+    ph_cases = []
+    for scheme, payoff, level, n0 in (("euler_maruyama", "identity", 3, 1), ("milstein", "call", 2, 2),
+                                      ("euler_maruyama", "identity", 0, 1), ("euler_maruyama", "identity", 5, 1)):
+        spec = mlmc.LevelSpec(level=level, scheme=scheme, process=gbm, rv_source=lin, kind="four_way",
+                              payoff=payoff, strike=1.0, n0=n0)
+        b = mlmc.simulate(spec, mlmc.level_stream(42, level), 1000, sides="both")
+        g[f"philox_gbm_{scheme}_{payoff}_l{level}_n{n0}"] = np.stack(
+            [b.p_fine_exact, b.p_coarse_exact, b.p_fine_approx, b.p_coarse_approx])
+        suite = mlmc.estimate_level_suite(spec, mlmc.level_stream(42, level), 1000)
+        g[f"philox_suite_{scheme}_{payoff}_l{level}_n{n0}"] = np.array(
+            [[suite[k].mean, suite[k].variance] for k in ("two_way_exact", "two_way_approx", "four_way")])
+        ph_cases.append([scheme, payoff, level, n0])
+    h["philox_gbm_cases"] = ph_cases
+
     # ------------------------------------------------------------------ CIR
     cir = mlmc.CirParams(kappa=0.5, theta=0.04, sigma=0.2, x0=0.04, t_end=1.0)
     from approxrv.tables import NcChi2Table  # noqa: F401
@@ -193,6 +218,12 @@ def mlmc_table(name):
 
     c = TABLES[name]
     return DyadicPolyTable(degree=c.shape[0] - 1, n_intervals=c.shape[1] - 1, coeffs=c)
+
+
+def ref_const_table():
+    from approxrv.tables import ConstantTable
+
+    return ConstantTable(q=10, values=TABLES["constant_q10_l1"], construction="l1")
 
 
 def ref_ncchi2_table(stacks_key, nu_key):

@@ -48,6 +48,24 @@ class TestPcg32:
         assert np.array_equal(u.astype(np.float64), (k.astype(np.float64) + 0.5) * 2.0**-23)
 
 
+class TestPhilox:
+    """The reference's own uniform source (UniformStream = numpy Philox-4x64-10)."""
+
+    def test_words_match_reference_stream(self, orc, golden):
+        assert np.array_equal(orc.philox_words(42, 7, 0, 64), golden["philox_words_42_7"])
+
+    def test_words_match_numpy_philox(self, orc):
+        from numpy.random import Philox
+
+        ref = Philox(key=np.array([3, 2**63 + 5], dtype=np.uint64), counter=0).random_raw(1003)
+        assert np.array_equal(orc.philox_words(3, 2**63 + 5, 0, 1003), ref)
+        assert np.array_equal(orc.philox_words(3, 2**63 + 5, 17, 986), ref[17:])
+
+    def test_uniforms_match_reference_stream(self, orc, golden):
+        u = orc.philox_uniforms(5, (3 << 32) | 1, 13, 4099)
+        assert np.array_equal(u, golden["philox_uniforms_5_3_c13"])
+
+
 class TestPluginKernels:
     def test_constant_eval(self, orc, golden, tables_npz):
         v = tables_npz["constant_q10_l1"]
