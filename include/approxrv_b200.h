@@ -180,7 +180,9 @@ ARV_API int64_t arv_mlmc_workspace_bytes(int64_t path_count);
 
 /* GBM (euler_maruyama / milstein, mlmc.py:164-229) and CIR truncated Euler
  * (mlmc.py:289-331) / truncated Milstein (new).  table: Gaussian dyadic
- * f64[degree+1][K1] (reference layout, dyadic_eval arithmetic). */
+ * f64[degree+1][K1] (reference layout, dyadic_eval arithmetic) for degree
+ * 1..5, or a piecewise-constant table values f64[K1] (constant_eval
+ * arithmetic) for degree 0; at most 48 KiB. */
 ARV_API int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, int degree, int64_t K1,
                             double *stats, double *paths, void *workspace, int64_t workspace_bytes,
                             void *stream);

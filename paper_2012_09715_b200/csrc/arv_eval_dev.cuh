@@ -18,6 +18,21 @@ __device__ __forceinline__ double dyadic_eval1(const double *c, int64_t K1, doub
     return pred ? z : -z;
 }
 
+// Approximate-side Gaussian table of the path kernels: DEG >= 1 is a dyadic
+// table (degree+1, K1) evaluated as dyadic_eval; DEG == 0 is a piecewise-
+// constant table values[K1] evaluated as constant_eval (_kernels.pyx:16-23).
+template <int DEG>
+__device__ __forceinline__ double gauss_table_eval(const double *c, int64_t K1, double u) {
+    if constexpr (DEG == 0) {
+        long long idx = static_cast<long long>(__dmul_rn(static_cast<double>(K1), u));
+        idx = idx < K1 ? idx : K1 - 1;
+        idx = idx < 0 ? 0 : idx;
+        return c[idx];
+    } else {
+        return dyadic_eval1<DEG>(c, K1, u);
+    }
+}
+
 // _kernels.pyx:96-143 for one element.  stacks (2, n_knots, DEG+1, K1):
 // upper half at 0, lower at 1; knot bracketing j = min(floor(sqrt(nu /
 // (lam + nu)) (n_knots - 1)), n_knots - 2); linear interpolation in t.

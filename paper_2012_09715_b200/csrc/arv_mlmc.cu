@@ -233,14 +233,14 @@ __global__ void __launch_bounds__(kLevelBlock) k_gaussian_level(LevelArgs A, con
             const double z1 = as241_f64(u1), z2 = as241_f64(u2);
             xf_e = step(step(xf_e, __dmul_rn(sq_f, z1), dt_f), __dmul_rn(sq_f, z2), dt_f);
             xc_e = step(xc_e, __dmul_rn(sq_f, __dadd_rn(z1, z2)), dt_c);
-            const double w1 = dyadic_eval1<DEG>(smd, K1, u1), w2 = dyadic_eval1<DEG>(smd, K1, u2);
+            const double w1 = gauss_table_eval<DEG>(smd, K1, u1), w2 = gauss_table_eval<DEG>(smd, K1, u2);
             xf_a = step(step(xf_a, __dmul_rn(sq_f, w1), dt_f), __dmul_rn(sq_f, w2), dt_f);
             xc_a = step(xc_a, __dmul_rn(sq_f, __dadd_rn(w1, w2)), dt_c);
         }
         if (A.n_f & 1) {
             const double u1 = rng.next();
             xf_e = step(xf_e, __dmul_rn(sq_f, as241_f64(u1)), dt_f);
-            xf_a = step(xf_a, __dmul_rn(sq_f, dyadic_eval1<DEG>(smd, K1, u1)), dt_f);
+            xf_a = step(xf_a, __dmul_rn(sq_f, gauss_table_eval<DEG>(smd, K1, u1)), dt_f);
         }
         const double fe = payoff_fn(xf_e, A.payoff, A.strike);
         const double fa = payoff_fn(xf_a, A.payoff, A.strike);
@@ -414,7 +414,9 @@ int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, in
     } else {
         return set_error(ARV_ERR_CONFIG, "arv_mlmc_gaussian_level cannot run scheme %d", scheme);
     }
-    if (K1 < 2 || K1 > 4096) return set_error(ARV_ERR_CONFIG, "bad table interval count");
+    // degree 0: piecewise-constant table values[K1]; >= 1: dyadic (degree+1, K1)
+    if (K1 < 2 || sizeof(double) * (degree + 1) * K1 > 48 * 1024)
+        return set_error(ARV_ERR_CONFIG, "table size out of range (degree %d, %lld columns)", degree, (long long)K1);
     if (spec->path_count < 1) return set_error(ARV_ERR_CONFIG, "need at least one path");
     const int64_t nb = n_blocks_for(spec->path_count);
     if (workspace_bytes < nb * 3 * ARV_NKIND * static_cast<int64_t>(sizeof(double)))
@@ -433,12 +435,13 @@ int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, in
         }                                                                                   \
         break;
     switch (degree) {
+        ARV_SCHEMES(0)
         ARV_SCHEMES(1)
         ARV_SCHEMES(2)
         ARV_SCHEMES(3)
         ARV_SCHEMES(4)
         ARV_SCHEMES(5)
-        default: return set_error(ARV_ERR_CONFIG, "polynomial degree must be in [1, 5], got %d", degree);
+        default: return set_error(ARV_ERR_CONFIG, "table degree must be in [0, 5], got %d", degree);
     }
 #undef ARV_SCHEMES
 #undef ARV_LAUNCH

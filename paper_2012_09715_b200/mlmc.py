@@ -186,11 +186,26 @@ _DEFAULT_GAUSS = "dyadic_linear_k15"
 def _gauss_coeffs(src) -> np.ndarray:
     if _is_exact(src):
         src = load_table(_DEFAULT_GAUSS)  # placeholder approx side; exact stats unaffected
-    if isinstance(src, SubDyadicTable) or isinstance(src, ConstantTable) or type(src).__name__ == "ConstantTable":
-        raise ConfigError("the device path kernels take dyadic (reference-layout) Gaussian tables")
+    if isinstance(src, ConstantTable) or type(src).__name__ == "ConstantTable":
+        # (1, 2^q): "degree 0" = piecewise constant, evaluated as constant_eval
+        v = np.asarray(src.values, dtype=np.float64).reshape(1, -1)
+        v.setflags(write=False)
+        return _cached_row(src, v)
+    if isinstance(src, SubDyadicTable):
+        raise ConfigError("the device path kernels take reference-layout Gaussian tables")
     if getattr(src, "decay", 0.5) != 0.5:
         raise ConfigError("the device path kernels require decay rate 1/2")
     return src.coeffs
+
+
+_ROWS: dict = {}
+
+
+def _cached_row(table, arr):
+    hit = _ROWS.get(id(table))
+    if hit is None or hit[0] is not table:
+        hit = _ROWS[id(table)] = (table, arr)
+    return hit[1]
 
 
 def _ncchi2_table(spec: LevelSpec):

@@ -153,3 +153,32 @@ def test_cir_statistical_targets(arv):
         assert 0.8e-3 < s["plain_exact"].variance < 1.25e-3  # closed form 1.01e-3
         gap = math.log2(s["correction"].variance / s["plain_exact"].variance)
         assert gap < -12.0, gap
+
+
+def test_gbm_constant_table_source(arv, orc, tables_npz):
+    """Piecewise-constant approximate side (evaluate -> constant_eval, sampler.py:97-108)."""
+    const = arv.load_table("constant_q10_l1")
+    spec = arv.LevelSpec(level=3, scheme="euler_maruyama", process=arv.GbmParams(**GBM), rv_source=const,
+                         kind="four_way", n0=1)
+    b = arv.simulate(spec, arv.level_stream(42, 3, generator="philox"), 2000)
+    # replay on the host with the oracle: the reference's UniformStream words + constant_eval + em_step
+    n, nf = 2000, 8
+    xf_a, xc_a = np.ones(n), np.ones(n)
+    dt, sq = 1.0 / nf, np.sqrt(1.0 / nf)
+    em = lambda x, dw, h: x * (1.0 + (0.05 * h + 0.2 * dw))  # noqa: E731  (mlmc.py:194-198)
+    for pair in range(nf // 2):
+        u1 = orc.philox_uniforms(42, 3 << 32, (2 * pair) * n, n)
+        u2 = orc.philox_uniforms(42, 3 << 32, (2 * pair + 1) * n, n)
+        w1, w2 = orc.constant_eval(const.values, u1), orc.constant_eval(const.values, u2)
+        xf_a = em(em(xf_a, sq * w1, dt), sq * w2, dt)
+        xc_a = em(xc_a, sq * (w1 + w2), 2.0 * dt)
+    assert np.array_equal(b.p_fine_approx.cpu().numpy(), xf_a)
+    assert np.array_equal(b.p_coarse_approx.cpu().numpy(), xc_a)
+    # test_mlmc.py:274-282: the 1024-value table drops the four-way variance by ~2^-13
+    gaps = []
+    for level in (2, 3, 4):
+        sp = arv.LevelSpec(level=level, scheme="euler_maruyama", process=arv.GbmParams(**GBM), rv_source=const,
+                           kind="four_way")
+        s = arv.estimate_level_suite(sp, arv.level_stream(29, level), 1 << 16)
+        gaps.append(math.log2(s["four_way"].variance / s["two_way_exact"].variance))
+    assert -15.0 <= float(np.mean(gaps)) <= -11.0
