@@ -24,6 +24,7 @@ from .sampler import (
     eval_subdyadic, evaluate, gaussian_inv_cdf, sample_coupled, shard_range,
 )
 from .tables import ConstantTable, DyadicPolyTable, NcChi2Table, SubDyadicTable, load_table, shipped_names
+from .tableio import export_table, import_table
 
 __all__ = [
     "ApproxRvError", "BadMagicError", "ChecksumError", "ConfigError", "DeviceError", "DomainError",
@@ -34,5 +35,6 @@ __all__ = [
     "CoupledGaussianBatch", "Pcg32Stream", "PhiloxStream", "dyadic_index", "eval_constant", "eval_dyadic", "eval_ncchi2",
     "eval_subdyadic", "evaluate", "gaussian_inv_cdf", "sample_coupled", "shard_range",
     "ConstantTable", "DyadicPolyTable", "NcChi2Table", "SubDyadicTable", "load_table", "shipped_names",
+    "export_table", "import_table",
     "backend_name", "get_kernels",
 ]

@@ -207,6 +207,18 @@ def main() -> None:
     h["config1_const_q10_f32_sha256_2^24"] = hc.hexdigest()
     h["dyadic_linear_k15_f32_sha256_2^24"] = hd.hexdigest()
 
+    # -------------------------------------- ARVT files written by the reference
+    from approxrv import tableio
+
+    arvt = os.path.join(HERE, "arvt")
+    os.makedirs(arvt, exist_ok=True)
+    nc16 = ref_ncchi2_table("ncchi2_cir_k16_stacks", "ncchi2_cir_k16_nu")
+    cubic = mlmc_table("dyadic_cubic_k15")
+    for name, tab in (("constant_q10", ref_const_table()), ("dyadic_linear_k15", lin), ("dyadic_cubic_k15", cubic),
+                      ("ncchi2_cir_k16", nc16)):
+        tableio.export_table(tab, os.path.join(arvt, f"{name}.arvt"))
+        tableio.export_table(tab, os.path.join(arvt, f"{name}.txt"), format="text")
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **g)
     with open(os.path.join(HERE, "hashes.json"), "w") as fh:
         json.dump(h, fh, indent=1)
