@@ -219,6 +219,15 @@ def main() -> None:
         tableio.export_table(tab, os.path.join(arvt, f"{name}.arvt"))
         tableio.export_table(tab, os.path.join(arvt, f"{name}.txt"), format="text")
 
+    # ------------------------------- the reference's MLMC experiment driver
+    from approxrv import cli
+
+    exp_cfg = {"process": "gbm", "scheme": "euler_maruyama", "seed": "42", "pilot": "4000", "epsilon": "0.01",
+               "levels": "0:4", "sources": "exact,linear:15", "n0": "2"}
+    cli.run_experiment(dict(exp_cfg), os.path.join(HERE, "experiment_ref"))
+    with open(os.path.join(HERE, "experiment_ref", "config.json"), "w") as fh:
+        json.dump(exp_cfg, fh, indent=1)
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **g)
     with open(os.path.join(HERE, "hashes.json"), "w") as fh:
         json.dump(h, fh, indent=1)
