@@ -219,6 +219,14 @@ def main() -> None:
         tableio.export_table(tab, os.path.join(arvt, f"{name}.arvt"))
         tableio.export_table(tab, os.path.join(arvt, f"{name}.txt"), format="text")
 
+    # ------------------------------------- Table-5 style RMSE grid (metrics.py:324-350)
+    from approxrv import metrics
+
+    grid = metrics.rmse_ncchi2([ref_ncchi2_table("ncchi2_nu1_k16_stacks", "ncchi2_nu1_k16_nu"), nc16_ref()],
+                               (1.0, 5.0, 10.0, 50.0, 100.0, 200.0), n_samples=1 << 14)
+    g["rmse_grid_values"] = grid.values
+    g["rmse_grid_lambdas"] = np.array(grid.lambdas)
+
     # ------------------------------- the reference's MLMC experiment driver
     from approxrv import cli
 
@@ -239,6 +247,10 @@ def mlmc_table(name):
 
     c = TABLES[name]
     return DyadicPolyTable(degree=c.shape[0] - 1, n_intervals=c.shape[1] - 1, coeffs=c)
+
+
+def nc16_ref():
+    return ref_ncchi2_table("ncchi2_cir_k16_stacks", "ncchi2_cir_k16_nu")
 
 
 def ref_const_table():

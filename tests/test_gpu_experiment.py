@@ -53,3 +53,19 @@ def test_nested_estimate_runs():
                                      [2000, 1000, 500, 250], seed=7)
     # E[X_T] under EM with 2^3 * 2 steps is (1 + 0.05/16)^16 ~ exp(0.05)
     assert abs(res["estimate"] - (1 + 0.05 / 16) ** 16) < 5 * res["std_error"] + 1e-4
+
+
+def test_device_rmse_grid_matches_reference(golden):
+    """metrics.rmse_ncchi2 (metrics.py:324-350) regenerated on the device."""
+    import numpy as np
+
+    import paper_2012_09715_b200 as arv
+    from paper_2012_09715_b200 import metrics
+
+    tabs = [arv.load_table("ncchi2_nu1_k16_stacks"), arv.load_table("ncchi2_cir_k16_stacks")]
+    grid = metrics.rmse_ncchi2(tabs, golden["rmse_grid_lambdas"], n_samples=1 << 14)
+    assert not grid.failures
+    # exact quantiles agree to the |F - u| <= 1e-9 tolerance of both Newton solvers
+    np.testing.assert_allclose(grid.values, golden["rmse_grid_values"], rtol=1e-6)
+    # published Table 5a, nu = 1 column (reproduce.py:30-37)
+    np.testing.assert_allclose(grid.values[:, 0], [0.036, 0.045, 0.054, 0.098, 0.134, 0.186], atol=0.0025)
