@@ -36,6 +36,8 @@ constexpr int kGenUnroll = ARV_GEN_UNROLL;
 static int g_group = 8;        // samples per thread-group: 4 (v4) or 8 (v8)
 static int g_ctas_per_sm = 8;  // resident CTAs per SM (256 threads each)
 
+constexpr int kJumpBits = 24;  // grid threads < 2^24
+
 struct GenArgs {
     uint64_t s_base;  // state whose output is sample 0 of this call
     uint64_t inc;
@@ -43,7 +45,17 @@ struct GenArgs {
     int64_t n;
     uint64_t zero;    // always 0: makes derived constants per-thread registers
     uint32_t zero32;
+    Affine pow2[kJumpBits];  // LCG^(G 2^i): a thread reaches group g0 with popcount(g0) steps
 };
+
+// State of the first sample of group g0 (g0 < 2^kJumpBits).
+__device__ __forceinline__ uint64_t group_start(const GenArgs &a, uint64_t g0) {
+    uint64_t s = a.s_base;
+#pragma unroll 1
+    for (int i = 0; i < kJumpBits; ++i)
+        if ((g0 >> i) & 1u) s = a.pow2[i].a * s + a.pow2[i].c;
+    return s;
+}
 
 static GenArgs make_gen_args(uint64_t seed, uint64_t stream_id, uint64_t offset, int64_t n,
                              int64_t total_threads, int G) {
@@ -55,6 +67,11 @@ static GenArgs make_gen_args(uint64_t seed, uint64_t stream_id, uint64_t offset,
     a.n = n;
     a.zero = 0;
     a.zero32 = 0;
+    Affine p = lcg_jump(static_cast<uint64_t>(G), st.inc);
+    for (int i = 0; i < kJumpBits; ++i) {
+        a.pow2[i] = p;
+        p = {p.a * p.a, p.a * p.c + p.c};  // compose the map with itself
+    }
     return a;
 }
 
@@ -75,6 +92,25 @@ struct VecOut<8> {
     }
 };
 
+// Evaluate two samples: the evaluator's packed-pair path when it has one.
+template <class Eval, class = void>
+struct HasPair {
+    static constexpr bool value = false;
+};
+template <class Eval>
+struct HasPair<Eval, decltype(void(Eval::kHasPair))> {
+    static constexpr bool value = Eval::kHasPair;
+};
+template <class Eval>
+__device__ __forceinline__ void eval_two(const Eval &eval, uint32_t w0, uint32_t w1, uint32_t &r0, uint32_t &r1) {
+    if constexpr (HasPair<Eval>::value) {
+        eval.pair(w0, w1, r0, r1);
+    } else {
+        r0 = eval(w0);
+        r1 = eval(w1);
+    }
+}
+
 // Drive `eval(w) -> uint32 bits` over the call's samples with G-wide stores
 // (out must be 4*G-byte aligned).
 template <int G, class Eval>
@@ -82,8 +118,7 @@ __device__ __forceinline__ void gen_loop_vec(const GenArgs &a, uint32_t *__restr
     const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t n_full = static_cast<uint64_t>(a.n) / G;
-    const Affine j0 = lcg_jump(static_cast<uint64_t>(G) * g0, a.inc);
-    uint64_t s = j0.a * a.s_base + j0.c;
+    uint64_t s = group_start(a, g0);
     const uint64_t z = static_cast<uint64_t>(threadIdx.x) * a.zero;  // 0, but not provably uniform
     const uint64_t inc = a.inc + z;
     const Affine st{a.stride.a + z, a.stride.c + z};
@@ -102,7 +137,7 @@ __device__ __forceinline__ void gen_loop_vec(const GenArgs &a, uint32_t *__restr
         }
         uint32_t r[G];
 #pragma unroll
-        for (int i = 0; i < G; ++i) r[i] = eval(w[i]);
+        for (int i = 0; i < G; i += 2) eval_two(eval, w[i], w[i + 1], r[i], r[i + 1]);
         VecOut<G>::store(p, r);
         p += step;
     }
@@ -203,6 +238,35 @@ struct EvalSubDyadic {
         }
         return __float_as_uint(z) ^ (~__float_as_uint(d) & 0x80000000u);
     }
+
+    // Two samples at once with sm_100's packed f32x2 FP instructions
+    // (FADD2 / FFMA2 / FMUL2: one issue slot for both lanes of the pair).
+    // Each lane is rounded exactly as the scalar path (IEEE rn, the product
+    // and the sum still separately rounded), so results are bit-identical.
+    static constexpr bool kHasPair = DEG == 1;
+    __device__ __forceinline__ void pair(uint32_t w0, uint32_t w1, uint32_t &r0, uint32_t &r1) const {
+        const uint64_t f = pack2(0x3F000000u | (w0 >> 9), 0x3F000000u | (w1 >> 9));
+        const uint64_t d = f32x2_fma(kTwo2, f32x2_add(f, kMinus075x2), kUlp24x2);  // u - 1/2, exact
+        const uint32_t d0 = lo32(d), d1 = hi32(d);
+        const uint64_t v = f32x2_add(kHalf2, pack2(d0 | 0x80000000u, d1 | 0x80000000u));  // 1/2 - |d|, exact
+        const uint32_t a0 = mad_u32(lo32(v) >> shift, four, base);
+        const uint32_t a1 = mad_u32(hi32(v) >> shift, four, base);
+        const uint64_t c1 = pack2(__float_as_uint(lds_f32<kLatticePlane * 4>(a0)),
+                                  __float_as_uint(lds_f32<kLatticePlane * 4>(a1)));
+        const uint64_t c0 = pack2(__float_as_uint(lds_f32<0>(a0)), __float_as_uint(lds_f32<0>(a1)));  // scalar use
+        // Product packed, sum scalar: ptxas contracts mul.rn.f32x2 + add.rn.f32x2
+        // into FFMA2 (one rounding), which would break parity with the
+        // reference's separately rounded z*v + c; FMUL2 + 2 FADD stays exact.
+        const uint64_t p = f32x2_mul(c1, v);
+        const float z0 = __fadd_rn(__uint_as_float(lo32(p)), __uint_as_float(lo32(c0)));
+        const float z1 = __fadd_rn(__uint_as_float(hi32(p)), __uint_as_float(hi32(c0)));
+        r0 = __float_as_uint(z0) ^ (~d0 & 0x80000000u);
+        r1 = __float_as_uint(z1) ^ (~d1 & 0x80000000u);
+    }
+    static constexpr uint64_t kTwo2 = 0x4000000040000000ull;       // {2, 2}
+    static constexpr uint64_t kMinus075x2 = 0xBF400000BF400000ull;  // {-0.75, -0.75}
+    static constexpr uint64_t kUlp24x2 = 0x3380000033800000ull;     // {2^-24, 2^-24}
+    static constexpr uint64_t kHalf2 = 0x3F0000003F000000ull;       // {0.5, 0.5}
 };
 
 // Stage natural-layout coeffs (DEG+1, K, nsub) into the lattice table.
