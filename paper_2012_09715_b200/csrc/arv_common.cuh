@@ -247,7 +247,9 @@ __device__ __forceinline__ float poly8f(int which, float x) {
     return acc;
 }
 
-__device__ __forceinline__ double as241_f64(double u) {
+// Reference-order evaluation, one branch per region (kept for the rare far
+// tail r > 5 and as the readable statement of exact_dist.py:87-126).
+__device__ __forceinline__ double as241_f64_branchy(double u) {
     const double q = __dsub_rn(u, 0.5);
     if (fabs(q) <= 0.425) {
         const double r = __dsub_rn(0.180625, __dmul_rn(q, q));
@@ -265,6 +267,38 @@ __device__ __forceinline__ double as241_f64(double u) {
         val = __ddiv_rn(poly8d(4, rf), poly8d(5, rf));
     }
     return upper ? val : -val;
+}
+
+// Same results, fewer divergent FP64 instructions: a warp almost always holds
+// both central and near-tail lanes (SURVEY §7 vi), so instead of executing
+// both rational functions it evaluates ONE degree-7/7 rational whose
+// coefficients are selected per lane (A/B central, C/D near tail) -- the
+// selects run on the otherwise idle integer pipe, the Horner steps and the
+// division keep the reference's operation order, so every lane is rounded
+// exactly as in as241_f64_branchy.  Only the log/sqrt of the tail and the
+// r > 5 far tail (u < ~1.4e-11) stay divergent.
+__device__ __forceinline__ double as241_f64(double u) {
+    const double q = __dsub_rn(u, 0.5);
+    const bool central = fabs(q) <= 0.425;
+    const bool upper = u > 0.5;
+    double x;
+    if (central) {
+        x = __dsub_rn(0.180625, __dmul_rn(q, q));
+    } else {
+        const double w = upper ? __dsub_rn(1.0, u) : u;
+        const double r = __dsqrt_rn(-log(w));
+        if (r > 5.0) return as241_f64_branchy(u);
+        x = __dsub_rn(r, 1.6);
+    }
+    double num = central ? kAS241d[0][7] : kAS241d[2][7];
+    double den = central ? kAS241d[1][7] : kAS241d[3][7];
+#pragma unroll
+    for (int i = 6; i >= 0; --i) {
+        num = __dadd_rn(__dmul_rn(num, x), central ? kAS241d[0][i] : kAS241d[2][i]);
+        den = __dadd_rn(__dmul_rn(den, x), central ? kAS241d[1][i] : kAS241d[3][i]);
+    }
+    const double val = __ddiv_rn(central ? __dmul_rn(q, num) : num, den);
+    return central || upper ? val : -val;
 }
 
 __device__ __forceinline__ float as241_f32(float u) {

@@ -24,6 +24,13 @@
 namespace arv {
 
 constexpr int kLevelBlock = 256;
+// Min resident CTAs per SM (register cap) for the level kernels; see sweeps.
+#ifndef ARV_GBM_MINB
+#define ARV_GBM_MINB 3
+#endif
+#ifndef ARV_CIR_MINB
+#define ARV_CIR_MINB 3
+#endif
 constexpr int kFinalBlock = 1024;
 
 struct LevelArgs {
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(kFinalBlock) k_finalize(const double *__restri
 // --------------------------------------------------- Gaussian schemes --
 // SCHEME: ARV_SCHEME_EM, _MILSTEIN (GBM), _CIR_EULER_TRUNCATED, _CIR_MILSTEIN_TRUNCATED
 template <int DEG, int SCHEME>
-__global__ void __launch_bounds__(kLevelBlock) k_gaussian_level(LevelArgs A, const double *__restrict__ coeffs,
+__global__ void __launch_bounds__(kLevelBlock, ARV_GBM_MINB) k_gaussian_level(LevelArgs A, const double *__restrict__ coeffs,
                                                                 int64_t K1, double *__restrict__ parts,
                                                                 double *__restrict__ paths) {
     extern __shared__ double smd[];
@@ -264,7 +271,7 @@ __global__ void __launch_bounds__(kLevelBlock) k_gaussian_level(LevelArgs A, con
 
 // ----------------------------------------------------------- CIR exact --
 template <int DEG>
-__global__ void __launch_bounds__(kLevelBlock) k_cir_exact_level(LevelArgs A, const double *__restrict__ stacks,
+__global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(LevelArgs A, const double *__restrict__ stacks,
                                                                  int64_t n_knots, int64_t K1, int use_smem,
                                                                  double *__restrict__ parts,
                                                                  double *__restrict__ paths,
