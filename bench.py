@@ -30,12 +30,24 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-N_PER_GPU = 1 << 28
-TABLE = "subdyadic_linear_k16_s8"
 BYTES_PER_SAMPLE = 4  # algorithmic: one f32 store, PRNG state in registers
 METRIC = "approx-Gaussian ICDF samples/s (fused PCG32, f32 out)"
-WORKLOAD = ("config2: PCG32(seed 42, stream 0) -> dyadic piecewise-linear ICDF, 16 octaves x 8 "
-            "sub-intervals per tail, degree-1 L2 fit, f32 out, 2^28 samples/GPU/step")
+WORKLOADS = {
+    # BASELINE.json configs[1] -- the headline (default)
+    "config2": (1 << 28, "subdyadic_linear_k16_s8",
+                "config2: PCG32(seed 42, stream 0) -> dyadic piecewise-linear ICDF, 16 octaves x 8 "
+                "sub-intervals per tail, degree-1 L2 fit, f32 out, 2^28 samples/GPU/step"),
+    # BASELINE.json configs[0] -- the reference's CPU-runnable case
+    "config1": (1 << 24, "constant_q10_l1",
+                "config1: PCG32(seed 42, stream 0) -> piecewise-constant ICDF, 2^10 equal intervals, "
+                "L1 (conditional-mean) values, f32 out, 2^24 samples/GPU/step"),
+}
+N_PER_GPU, TABLE, WORKLOAD = WORKLOADS["config2"]
+
+
+def select_workload(name: str) -> None:
+    global N_PER_GPU, TABLE, WORKLOAD
+    N_PER_GPU, TABLE, WORKLOAD = WORKLOADS[name]
 
 
 def _peaks() -> dict:
@@ -116,10 +128,14 @@ def cpu_port_rate(total: int, threads: int) -> tuple[float, float]:
     per = max(4, (total // threads) & ~3)
     bufs = [np.empty(per, dtype=np.float32) for _ in range(threads)]
     cptr = c.ctypes.data_as(oracle.oracle.C.c_void_p)
+    vp = oracle.oracle.C.c_void_p
 
     def work(i):
-        oracle.lib.orc_pcg32_subdyadic_f32(42, 0, i * per, cptr, 1, 16, 3,
-                                           bufs[i].ctypes.data_as(oracle.oracle.C.c_void_p), per)
+        o = bufs[i].ctypes.data_as(vp)
+        if TABLE.startswith("constant"):
+            oracle.lib.orc_pcg32_constant_f32(42, 0, i * per, cptr, int(np.log2(c.size)), o, per)
+        else:
+            oracle.lib.orc_pcg32_subdyadic_f32(42, 0, i * per, cptr, 1, 16, 3, o, per)
 
     with ThreadPoolExecutor(threads) as ex:
         t0 = time.perf_counter()
@@ -147,8 +163,44 @@ def cpu_baseline(target_seconds: float = 8.0) -> dict:
     except Exception:
         pass
     return {"value": rate, "unit": "samples/s", "cores": threads, "kind": "port",
-            "sample": f"{total} samples of the config-2 workload (oracle/oracle.c PCG32 + 16x8 sub-interval "
-                      f"evaluator, -O3 generic x86-64, no FMA), {threads} threads, {dt:.2f} s; CPU: {model}"}
+            "sample": f"{total} samples of the {WORKLOAD.split(':')[0]} workload (oracle/oracle.c PCG32 + the same "
+                      f"table evaluator, -O3 generic x86-64, no FMA), {threads} threads, {dt:.2f} s; CPU: {model}"}
+
+
+def _ref_kernel_worker(args):
+    """One process: the reference's compiled dyadic_eval32 (oracle/_ref) on a chunk."""
+    offset, n, reps = args
+    import oracle
+
+    ref = oracle.load_ref_kernels()
+    c = np.load(os.path.join(REPO, "paper_2012_09715_b200", "data", "tables.npz"))["dyadic_linear_k15"]
+    c32 = c.astype(np.float32)
+    u = oracle.u32_to_f32(oracle.pcg32_words(42, 0, offset, n))
+    out = np.empty_like(u)
+    ref.dyadic_eval32(c32, u, out)  # warm
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        ref.dyadic_eval32(c32, u, out)
+    return n * reps, time.perf_counter() - t0
+
+
+def reference_kernel_rate(procs: int, n_per_proc: int = 1 << 22, reps: int = 3) -> dict | None:
+    """The reference's own Cython kernel (compiled from /root/reference into oracle/_ref),
+    dyadic_eval32 on the K15 table over the same PCG32 lattice uniforms, one process
+    per core (the Cython loop holds the GIL).  Uniform generation is excluded."""
+    import multiprocessing as mp
+
+    import oracle
+
+    if oracle.load_ref_kernels() is None:
+        return None
+    with mp.get_context("spawn").Pool(procs) as pool:
+        res = pool.map(_ref_kernel_worker, [(i * n_per_proc, n_per_proc, reps) for i in range(procs)])
+    samples = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return {"value": samples / wall, "unit": "samples/s", "cores": procs, "kind": "reference",
+            "sample": f"oracle/_ref _kernels.dyadic_eval32 (reference Cython, -O3) on the K15 linear table, "
+                      f"{procs} processes x {reps} x {n_per_proc} PCG32 lattice uniforms (generation excluded)"}
 
 
 # ---------------------------------------------------------------------------
@@ -159,7 +211,7 @@ def run_reference(args) -> None:
     if int(os.environ.get("RANK", "0")) != 0:
         return
     threads = cpu_threads()
-    per_step = 1 << 26
+    per_step = min(1 << 26, N_PER_GPU)
     for _ in range(max(args.warmup, 0)):
         cpu_port_rate(per_step, threads)
     t0 = time.perf_counter()
@@ -177,6 +229,12 @@ def run_reference(args) -> None:
                          "sample": f"{per_step} samples per step, {threads} threads, oracle/oracle.c"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        rk = reference_kernel_rate(threads)
+    except Exception as exc:  # the context figure must never break the arm
+        rk = {"unavailable": f"{type(exc).__name__}: {exc}"}
+    if rk is not None:
+        line["reference_kernel"] = rk
     print(json.dumps(line), flush=True)
 
 
@@ -228,19 +286,37 @@ def run_ours(args) -> None:
 
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(device.index)
+    # Outputs smaller than L2 (config 1: 64 MiB) are timed launch by launch
+    # with a 512 MiB store sweep flushing L2 between launches (outside the
+    # events); larger outputs stream straight through L2.
+    flush = n * 4 < (256 << 20)
+    scratch = torch.empty(128 << 20, dtype=torch.float32, device=device) if flush else None
     barrier()
     torch.cuda.synchronize()
     l0 = _native.launch_count()
+    elapsed = 0.0
     with sampler:
-        start.record()
-        for _ in range(args.steps):
-            step()
-        stop.record()
-        stop.synchronize()
-    launches = _native.launch_count() - l0
+        if flush:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            s = torch.cuda.current_stream().cuda_stream
+            for a, b in evs:
+                _native.call("arv_store_probe", scratch.data_ptr(), scratch.numel(), s)
+                a.record()
+                step()
+                b.record()
+            torch.cuda.synchronize()
+            elapsed = sum(a.elapsed_time(b) for a, b in evs) * 1e-3
+        else:
+            start.record()
+            for _ in range(args.steps):
+                step()
+            stop.record()
+            stop.synchronize()
+            elapsed = start.elapsed_time(stop) * 1e-3
+    launches = _native.launch_count() - l0 - (args.steps if flush else 0)
     barrier()
     torch.cuda.synchronize()
-    elapsed = start.elapsed_time(stop) * 1e-3
     t = torch.tensor([elapsed], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -299,7 +375,8 @@ def run_ours(args) -> None:
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (PCG32 stream, no dataset)",
         "config": {"workload": WORKLOAD, "table": TABLE, "samples_per_gpu_per_step": n,
                    "parallelism": f"dp{world} (PCG32 offset shards, no data-path collective)",
-                   "l2": "output 1 GiB per GPU per step > 126 MB L2 (inputs larger than L2; no flush needed)"},
+                   "l2": ("output 1 GiB per GPU per step > 126 MB L2 (no flush needed)" if n * 4 >= (256 << 20) else
+                          "output < L2: each launch timed alone, 512 MiB store sweep flushes L2 in between")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": _load_traffic(), "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": n * BYTES_PER_SAMPLE,
@@ -381,7 +458,9 @@ def main() -> None:
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-mlmc", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config2")
     args = ap.parse_args()
+    select_workload(args.workload)
     if args.impl == "reference":
         run_reference(args)
     else:
