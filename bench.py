@@ -242,13 +242,16 @@ def run_reference(args) -> None:
 # our arm
 # ---------------------------------------------------------------------------
 
-def _load_traffic() -> float | None:
-    """dram bytes/launch of the dominant kernel from the committed ncu summary, if any."""
+def _load_traffic(n: int) -> float | None:
+    """DRAM bytes per launch of this workload's kernel from the committed ncu
+    capture (profiles/ncu_summary.json, measured at its own sample count and
+    scaled per sample), or None."""
     p = os.path.join(REPO, "profiles", "ncu_summary.json")
+    key = "constant" if TABLE.startswith("constant") else "subdyadic"
     try:
         with open(p) as fh:
-            d = json.load(fh)
-        return d.get("subdyadic", {}).get("dram_bytes_per_launch")
+            d = json.load(fh)[key]
+        return d["dram_bytes_per_launch"] / d["samples_per_launch"] * n
     except Exception:
         return None
 
@@ -378,7 +381,7 @@ def run_ours(args) -> None:
                    "l2": ("output 1 GiB per GPU per step > 126 MB L2 (no flush needed)" if n * 4 >= (256 << 20) else
                           "output < L2: each launch timed alone, 512 MiB store sweep flushes L2 in between")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": _load_traffic(), "peak_source": peak_src,
+                     "traffic": _load_traffic(n), "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": n * BYTES_PER_SAMPLE,
                      "store_only_probe_gbs": store_gbs, "frac_of_store_probe": achieved / store_gbs},
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": 0,
