@@ -264,8 +264,15 @@ def run_ours(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # ARV_BENCH_DIST_BACKEND=gloo exercises the multi-rank code path on a box
+        # with fewer GPUs (ranks share devices; gloo syncs on the host, so no GPU
+        # kernel ever waits on another rank).  Production runs use NCCL.
+        backend = os.environ.get("ARV_BENCH_DIST_BACKEND", "nccl")
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     device = torch.device("cuda", torch.cuda.current_device())
 
     import paper_2012_09715_b200 as arv

@@ -108,6 +108,35 @@ class TestFusedGenerators:
         # antisymmetry on the lattice is structural: the top and bottom halves are mirror images
         assert bool(torch.isfinite(out).all())
 
+    @pytest.mark.parametrize("n", [1, 2, 7, 8, 9, 15, 31, 33, 1023, 4097])
+    @pytest.mark.parametrize("pad", [0, 1, 4])  # element offset into the buffer: v8 / scalar / v4 store paths
+    def test_small_and_ragged(self, arv, orc, tables_npz, n, pad):
+        sub = arv.load_table("subdyadic_linear_k16_s8")
+        const = arv.load_table("constant_q10_l1")
+        buf = torch.full((n + 16,), float("nan"), dtype=torch.float32, device="cuda")
+        arv.Pcg32Stream(9, 4, counter=5).sample(sub, n, out=buf[pad:pad + n])
+        ref = orc.pcg32_subdyadic_f32(9, 4, 5, tables_npz["subdyadic_linear_k16_s8"].astype(np.float32), 3, n)
+        assert np.array_equal(bits(buf[pad:pad + n]), bits(ref))
+        assert bool(torch.isnan(buf[pad + n:]).all()) and bool(torch.isnan(buf[:pad]).all())  # no overrun
+        arv.Pcg32Stream(9, 4, counter=5).sample(const, n, out=buf[pad:pad + n])
+        ref = orc.pcg32_constant_f32(9, 4, 5, tables_npz["constant_q10_l1"], n)
+        assert np.array_equal(bits(buf[pad:pad + n]), bits(ref))
+
+    def test_all_group_sizes_agree(self, arv):
+        from paper_2012_09715_b200 import _native
+
+        t = arv.load_table("subdyadic_linear_k16_s8")
+        outs = []
+        try:
+            for group, ctas in ((8, 8), (4, 8), (8, 2), (4, 1)):
+                _native.call("arv_set_tuning", 1, group)
+                _native.call("arv_set_tuning", 2, ctas)
+                outs.append(arv.Pcg32Stream(42, 0, counter=77).sample(t, 300001).cpu().numpy())
+        finally:
+            _native.call("arv_set_tuning", 1, 8)
+            _native.call("arv_set_tuning", 2, 8)
+        assert all(np.array_equal(bits(o), bits(outs[0])) for o in outs[1:])
+
     def test_unaligned_output(self, arv, orc, tables_npz):
         buf = torch.empty(10001, dtype=torch.float32, device="cuda")
         arv.Pcg32Stream(42, 0).sample(arv.load_table("subdyadic_linear_k16_s8"), 10000, out=buf[1:])
