@@ -12,6 +12,7 @@
 from __future__ import annotations
 
 import threading
+from collections import OrderedDict
 
 import numpy as np
 import torch
@@ -69,7 +70,8 @@ def _torch_to_np(dtype: torch.dtype):
     raise ConfigError(f"unsupported dtype {dtype}")
 
 
-_table_cache: dict = {}
+_TABLE_CACHE_MAX = 64  # device copies of distinct read-only tables kept (LRU)
+_table_cache: "OrderedDict" = OrderedDict()
 _table_lock = threading.Lock()
 
 
@@ -86,9 +88,12 @@ def table_on_device(arr, dtype: torch.dtype, device: torch.device | None = None)
     with _table_lock:
         hit = _table_cache.get(key)
         if hit is not None and hit[0] is a:
+            _table_cache.move_to_end(key)
             return hit[1]
         t = to_device(a, dtype, device)
-        _table_cache[key] = (a, t)
+        _table_cache[key] = (a, t)  # holds `a`, so its buffer address cannot be reused while cached
+        while len(_table_cache) > _TABLE_CACHE_MAX:
+            _table_cache.popitem(last=False)
         return t
 
 

@@ -446,9 +446,14 @@ def _natural32(table) -> np.ndarray:
     return hit[1]
 
 
-def sample_coupled(stream: Pcg32Stream, table, n: int) -> CoupledGaussianBatch:
-    """Draw n uniforms once; exact and approximate Gaussians (sampler.py:209-218)."""
-    u = stream.uniforms(n, dtype=np.float64)
+def sample_coupled(stream, table, n: int) -> CoupledGaussianBatch:
+    """Draw n uniforms once; exact and approximate Gaussians (sampler.py:209-218).
+
+    ``stream`` is a Pcg32Stream (f64 uniforms (w + 0.5) 2^-32) or a
+    PhiloxStream (the reference's own UniformStream uniforms, so the pair
+    matches the reference's sample_coupled bit for bit on the table side).
+    """
+    u = stream.uniforms(n) if isinstance(stream, PhiloxStream) else stream.uniforms(n, dtype=np.float64)
     z_exact = torch.empty_like(u)
     kernels.gaussian_inv_cdf(u, z_exact)
     z_approx = evaluate(table, u)

@@ -50,6 +50,15 @@ def test_fused_evaluate_matches_reference(arv, golden):
     np.testing.assert_allclose(ex, ref, rtol=1e-14, atol=0)
 
 
+def test_sample_coupled_matches_reference(arv, golden):
+    """sampler.sample_coupled (sampler.py:209-218) on the reference's own stream."""
+    lin = arv.load_table("dyadic_linear_k15")
+    b = arv.sample_coupled(arv.PhiloxStream(42, 9), lin, 8192)
+    assert np.array_equal(bits(b.z_approx), bits(golden["philox_eval_dyadic_lin"]))
+    np.testing.assert_allclose(b.z_exact.cpu().numpy(), golden["philox_eval_exact"], rtol=1e-14, atol=0)
+    assert len(b) == 8192
+
+
 def test_gbm_replays_reference_paths(arv, golden, hashes):
     lin = arv.load_table("dyadic_linear_k15")
     gbm = arv.GbmParams(0.05, 0.2, 1.0, 1.0)
