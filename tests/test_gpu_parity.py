@@ -241,3 +241,25 @@ class TestDropInKernels:
         before = _native.launch_count()
         arv.Pcg32Stream(1, 1).sample(arv.load_table("constant_q10_l1"), 1000)
         assert _native.launch_count() == before + 1
+
+
+def test_standalone_c_client(tmp_path, orc, tables_npz):
+    """examples/c_abi_demo.c: a plain C program (no Python/torch) drives the C ABI."""
+    import os
+    import subprocess
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "c_abi_demo"
+    subprocess.run(["gcc", "-O2", "-I", os.path.join(repo, "include"), "-I", "/usr/local/cuda/include",
+                    os.path.join(repo, "examples", "c_abi_demo.c"),
+                    "-L", os.path.join(repo, "paper_2012_09715_b200"), "-larv_b200", "-L", "/usr/local/cuda/lib64",
+                    "-lcudart", f"-Wl,-rpath,{os.path.join(repo, 'paper_2012_09715_b200')}", "-o", str(exe)],
+                   check=True)
+    c = tables_npz["subdyadic_linear_k16_s8"].astype(np.float32)
+    (tmp_path / "t.f32").write_bytes(c.tobytes())
+    n = 1000003
+    r = subprocess.run([str(exe), str(tmp_path / "t.f32"), str(n), str(tmp_path / "o.f32")], capture_output=True,
+                       text=True)
+    assert r.returncode == 0, r.stderr
+    got = np.fromfile(tmp_path / "o.f32", dtype=np.float32)
+    assert np.array_equal(bits(got), bits(orc.pcg32_subdyadic_f32(42, 0, 0, c, 3, n)))
