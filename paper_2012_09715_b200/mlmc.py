@@ -300,6 +300,13 @@ def merge_triples(parts: np.ndarray) -> np.ndarray:
     return out
 
 
+def _host_if_gloo(t: torch.Tensor, group=None) -> torch.Tensor:
+    """gloo reduces host tensors; NCCL keeps them on the device."""
+    import torch.distributed as dist
+
+    return t.cpu() if dist.get_backend(group) == "gloo" else t
+
+
 def allreduce_triples(triples: torch.Tensor, group=None) -> torch.Tensor:
     """Merge per-rank (count, mean, M2) rows across a torch.distributed group.
 
@@ -309,7 +316,7 @@ def allreduce_triples(triples: torch.Tensor, group=None) -> torch.Tensor:
     """
     import torch.distributed as dist
 
-    t = triples.to(torch.float64)
+    t = _host_if_gloo(triples.to(torch.float64), group)
     n = t[:, 0].clone()
     s1 = torch.stack([n, n * t[:, 1]], dim=1).contiguous()
     dist.all_reduce(s1, group=group)
@@ -345,7 +352,12 @@ def _timed_level(spec, stream, n_pilot, group=None):
     stats, _, n_fail = run_level(spec, stream, n_pilot, path_lo=lo, path_count=cnt, device=device)
     stop.record()
     if world > 1:
+        import torch.distributed as dist
+
         stats = allreduce_triples(stats, group)
+        if n_fail is not None:  # every rank raises if any rank's transitions failed
+            n_fail = _host_if_gloo(n_fail, group)
+            dist.all_reduce(n_fail, group=group)
     stop.synchronize()
     _check_fail(spec, n_fail)
     seconds = start.elapsed_time(stop) * 1e-3
