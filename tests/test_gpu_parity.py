@@ -235,6 +235,39 @@ class TestDropInKernels:
         with pytest.raises(arv.DomainError):
             arv.gaussian_inv_cdf(np.array([0.0, 0.5]))
 
+    def test_fuzz_bit_patterns(self, arv, orc, tables_npz):
+        """Random f64/f32 bit patterns in [0, 1] incl. subnormals, 0, 1/2 neighbours and
+        exact powers of two: the drop-in kernels equal the oracle restatement (itself
+        pinned to the reference) everywhere in the (0, 1) contract and never fault
+        outside it (negative / > 1 / NaN inputs)."""
+        k = arv.get_kernels()
+        rng = np.random.default_rng(2024)
+        raw = rng.integers(0, 0x3FF0000000000000, size=200_000, dtype=np.uint64)
+        u = raw.view(np.float64).copy()
+        u[:64] = [0.0, 1.0, 0.5, np.nextafter(0.5, 0), np.nextafter(0.5, 1), 5e-324, 2.0**-1022, 2.0**-1074] + \
+            [2.0 ** -e for e in range(1, 57)]
+        for name in ("dyadic_linear_k15", "dyadic_cubic_k15"):
+            out = np.empty_like(u)
+            k.dyadic_eval(tables_npz[name], u, out)
+            inside = (u > 0) & (u < 1)
+            assert np.array_equal(bits(out[inside]), bits(orc.dyadic_eval(tables_npz[name], u[inside])))
+        assert np.array_equal(k.dyadic_index(u, 40), orc.dyadic_index(u, 40))
+        u32 = raw.astype(np.uint32).view(np.float32)
+        u32 = np.where((u32 >= 0) & (u32 <= 1), u32, np.float32(0.25)).astype(np.float32)
+        out32 = np.empty_like(u32)
+        k.dyadic_eval32(tables_npz["dyadic_linear_k15"].astype(np.float32), u32, out32)
+        inside = (u32 > 0) & (u32 < 1)
+        ref = orc.dyadic_eval32(tables_npz["dyadic_linear_k15"].astype(np.float32), u32[inside])
+        assert np.array_equal(bits(out32[inside]), bits(ref))
+        assert np.array_equal(k.dyadic_index32(u32, 15), orc.dyadic_index32(u32, 15))
+        # out of contract: must not fault, values unspecified
+        bad = np.array([-0.5, 1.5, np.nan, np.inf, -np.inf, -0.0, 2.0], dtype=np.float64)
+        out = np.empty_like(bad)
+        k.dyadic_eval(tables_npz["dyadic_linear_k15"], bad, out)
+        k.constant_eval(tables_npz["constant_q10_l1"], bad, out)
+        k.ncchi2_eval(tables_npz["ncchi2_cir_k64_stacks"], 2.0, bad, np.array([1.0]), out)
+        torch.cuda.synchronize()
+
     def test_launch_counter_advances(self, arv):
         from paper_2012_09715_b200 import _native
 
