@@ -233,6 +233,13 @@ static __constant__ double kAS241d[6][8] = {{ARV_AS241_A}, {ARV_AS241_B}, {ARV_A
 static __constant__ float kAS241f[6][8] = {{ARV_AS241_A}, {ARV_AS241_B}, {ARV_AS241_C},
                                            {ARV_AS241_D}, {ARV_AS241_E}, {ARV_AS241_F}};
 
+// A|B|C|D rows (central num/den, near-tail num/den) in global memory for the
+// per-lane coefficient loads of as241_f64.
+#ifndef ARV_AS241_SELECT
+#define ARV_AS241_SELECT 0
+#endif
+static __device__ const double kAS241g[32] = {ARV_AS241_A, ARV_AS241_B, ARV_AS241_C, ARV_AS241_D};
+
 // Horner with separately rounded multiply and add (numpy has no FMA).
 __device__ __forceinline__ double poly8d(int which, double x) {
     double acc = kAS241d[which][7];
@@ -290,6 +297,7 @@ __device__ __forceinline__ double as241_f64(double u) {
         if (r > 5.0) return as241_f64_branchy(u);
         x = __dsub_rn(r, 1.6);
     }
+#if ARV_AS241_SELECT
     double num = central ? kAS241d[0][7] : kAS241d[2][7];
     double den = central ? kAS241d[1][7] : kAS241d[3][7];
 #pragma unroll
@@ -297,11 +305,24 @@ __device__ __forceinline__ double as241_f64(double u) {
         num = __dadd_rn(__dmul_rn(num, x), central ? kAS241d[0][i] : kAS241d[2][i]);
         den = __dadd_rn(__dmul_rn(den, x), central ? kAS241d[1][i] : kAS241d[3][i]);
     }
+#else
+    // per-lane coefficient row from the read-only path: one LDG per
+    // coefficient (<= 2 distinct addresses per warp, L1-resident) instead of
+    // two integer selects per coefficient
+    const double *cf = kAS241g + (central ? 0 : 16);
+    double num = __ldg(cf + 7);
+    double den = __ldg(cf + 15);
+#pragma unroll
+    for (int i = 6; i >= 0; --i) {
+        num = __dadd_rn(__dmul_rn(num, x), __ldg(cf + i));
+        den = __dadd_rn(__dmul_rn(den, x), __ldg(cf + 8 + i));
+    }
+#endif
     const double val = __ddiv_rn(central ? __dmul_rn(q, num) : num, den);
     return central || upper ? val : -val;
 }
 
-__device__ __forceinline__ float as241_f32(float u) {
+__device__ __forceinline__ float as241_f32_branchy(float u) {
     const float q = __fsub_rn(u, 0.5f);
     if (fabsf(q) <= 0.425f) {
         const float r = __fsub_rn(0.180625f, __fmul_rn(q, q));
@@ -319,6 +340,34 @@ __device__ __forceinline__ float as241_f32(float u) {
         val = __fdiv_rn(poly8f(4, rf), poly8f(5, rf));
     }
     return upper ? val : -val;
+}
+
+static __device__ const float kAS241gf[32] = {ARV_AS241_A, ARV_AS241_B, ARV_AS241_C, ARV_AS241_D};
+
+// Same results as as241_f32_branchy with one rational per lane (see as241_f64).
+__device__ __forceinline__ float as241_f32(float u) {
+    const float q = __fsub_rn(u, 0.5f);
+    const bool central = fabsf(q) <= 0.425f;
+    const bool upper = u > 0.5f;
+    float x;
+    if (central) {
+        x = __fsub_rn(0.180625f, __fmul_rn(q, q));
+    } else {
+        const float w = upper ? __fsub_rn(1.0f, u) : u;
+        const float r = __fsqrt_rn(-logf(w));
+        if (r > 5.0f) return as241_f32_branchy(u);
+        x = __fsub_rn(r, 1.6f);
+    }
+    const float *cf = kAS241gf + (central ? 0 : 16);
+    float num = __ldg(cf + 7);
+    float den = __ldg(cf + 15);
+#pragma unroll
+    for (int i = 6; i >= 0; --i) {
+        num = __fadd_rn(__fmul_rn(num, x), __ldg(cf + i));
+        den = __fadd_rn(__fmul_rn(den, x), __ldg(cf + 8 + i));
+    }
+    const float val = __fdiv_rn(central ? __fmul_rn(q, num) : num, den);
+    return central || upper ? val : -val;
 }
 
 // ------------------------------------------------- dyadic index helpers --
