@@ -256,6 +256,26 @@ def _load_traffic(n: int) -> float | None:
         return None
 
 
+def _fp64_roofline(key: str, path_steps_per_s: float) -> dict | None:
+    """FP64 roofline of an MLMC level kernel: achieved = FP64 FLOP per path-step
+    (ncu dadd + dmul + 2 dfma of the committed capture, profiles/ncu_summary.json)
+    x measured path-steps/s; peak = 64 DFMA lanes/SM/clk x 2 x SMs x max SM clock."""
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_summary.json")) as fh:
+            d = json.load(fh)[key]
+        import torch
+
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        mhz = _peaks().get("sm_max_mhz", 1965.0)
+        peak = 64 * 2 * sms * mhz * 1e6 / 1e12
+        achieved = d["dp_flops_per_path_step"] * path_steps_per_s / 1e12
+        return {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "flops_per_path_step": d["dp_flops_per_path_step"], "fp64_pipe_active_pct_ncu": d["fp64_pipe_active_pct"],
+                "peak_source": "nominal: ncu peak_sustained 64 DFMA/SM/clk x max SM clock (MEASURED_PEAKS sm_max_mhz)"}
+    except Exception:
+        return None
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -448,6 +468,8 @@ def mlmc_metrics(arv, args, rank, world, device) -> dict:
         paths_total = n_paths * len(levels)
         entry = {"paths_per_level": n_paths, "levels": [levels[0], levels[-1]], "seconds": secs,
                  "paths_per_s": paths_total / secs, "path_steps_per_s": n_paths * steps / secs}
+        entry["roofline"] = _fp64_roofline("gbm_level8" if scheme != "cir_exact" else "cir_level6",
+                                           n_paths * steps / secs)
         s = [x[0].cpu().numpy() for x in stats]
         if scheme == "cir_exact":
             entry["n_fail"] = int(sum(int(x[1].item()) for x in stats))
