@@ -269,7 +269,10 @@ def _fp64_roofline(key: str, path_steps_per_s: float) -> dict | None:
         mhz = _peaks().get("sm_max_mhz", 1965.0)
         peak = 64 * 2 * sms * mhz * 1e6 / 1e12
         achieved = d["dp_flops_per_path_step"] * path_steps_per_s / 1e12
+        # DADD/DMUL occupy a DFMA lane for 1 FLOP, so also report FP64 lane-op issue vs the lane peak
+        lane_frac = d["dp_lane_ops_per_path_step"] * path_steps_per_s / (64 * sms * mhz * 1e6)
         return {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "fp64_lane_op_frac": lane_frac,
                 "flops_per_path_step": d["dp_flops_per_path_step"], "fp64_pipe_active_pct_ncu": d["fp64_pipe_active_pct"],
                 "peak_source": "nominal: ncu peak_sustained 64 DFMA/SM/clk x max SM clock (MEASURED_PEAKS sm_max_mhz)"}
     except Exception:
