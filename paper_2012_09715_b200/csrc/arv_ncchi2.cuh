@@ -79,10 +79,23 @@ __device__ inline GammaPQ gamma_pq(const NcTables &t, long long k, double y, dou
     if (y < a + 1.0) {
         // P = G * sum_{n>=0} y^n / ((a+1)...(a+n)),  1/(a+n) = 1/(a0+k+n)
         double sum = 1.0, term = 1.0;
-        for (long long n = 1; n < 4000; ++n) {
-            term *= y * t.raj(k + n);
+        int n = static_cast<int>(k) + 1;
+        bool done = false;
+        for (; n < kNcTab; ++n) {  // 1/(a0 + n) from the table
+            term *= y * t.inv_aj[n];
             sum += term;
-            if (term < sum * 1e-17) break;
+            if (term < sum * 1e-17) {
+                done = true;
+                break;
+            }
+        }
+        if (!done) {
+            double an = t.a0 + static_cast<double>(n);
+            for (int guard = 0; guard < 4000; ++guard, an += 1.0) {
+                term *= y / an;
+                sum += term;
+                if (term < sum * 1e-17) break;
+            }
         }
         r.small = G * sum;
         r.lower = true;
@@ -116,6 +129,57 @@ struct NcCdf {
     double pdf;
 };
 
+// Poisson window forward from the mode, j = k+1, k+2, ...: the carried side
+// S_j (P_j if LOWER, Q_j otherwise) changes by G_{j-1} = G(a0 + j - 1), which
+// is also the density term.  The table phase (j < kNcTab) is multiply/add
+// only; a second loop with divisions covers windows past the tables.  Loop
+// counters stay 32-bit and j is tracked as a double (no I2F per term).
+template <bool LOWER>
+__device__ __forceinline__ void nc_forward(const NcTables &t, long long k, double kd, double h, double y, double pk,
+                                           double S, double G, double &wsum, double &acc, double &dens) {
+    double p = pk, jd = kd;
+    int j = static_cast<int>(k) + 1;
+    for (; j < kNcTab; ++j) {
+        jd += 1.0;
+        p *= h * t.inv_j[j];
+        S = LOWER ? fmax(S - G, 0.0) : S + G;
+        dens += p * G;
+        G *= y * t.inv_aj[j];
+        wsum += p;
+        acc += p * S;
+        if (p < 1e-18 && jd > h) return;
+    }
+    for (int guard = 0; guard < 200000; ++guard) {
+        jd += 1.0;
+        p *= h / jd;
+        S = LOWER ? fmax(S - G, 0.0) : S + G;
+        dens += p * G;
+        G *= y / (t.a0 + jd);
+        wsum += p;
+        acc += p * S;
+        if (p < 1e-18 && jd > h) return;
+    }
+}
+
+// Backward from the mode, j = k-1, ..., 0: G_j = G_{j+1} (a0 + j + 1) / y,
+// the carried side changes by G_j, the density term is G_{j-1}.
+template <bool LOWER>
+__device__ __forceinline__ void nc_backward(double a0, long long k, double kd, double inv_h, double inv_y, double pk,
+                                            double S, double G, double &wsum, double &acc, double &dens) {
+    double p = pk, jd = kd;  // jd = j + 1 at the top of each iteration
+    for (long long j = k - 1; j >= 0; --j) {
+        p *= jd * inv_h;
+        const double aj = a0 + jd;  // a0 + j + 1
+        G *= aj * inv_y;
+        S = LOWER ? S + G : fmax(S - G, 0.0);
+        wsum += p;
+        acc += p * S;
+        dens += p * G * (aj - 1.0) * inv_y;
+        jd -= 1.0;
+        if (p < 1e-18) return;
+    }
+}
+
 // F(x) - u and f(x) for x > 0.  `one_minus_u` is exact for u >= 1/2.
 __device__ inline NcCdf ncchi2_cdf_minus(const NcTables &t, double x, double lam, double u, double one_minus_u) {
     const double y = 0.5 * x;
@@ -135,33 +199,12 @@ __device__ inline NcCdf ncchi2_cdf_minus(const NcTables &t, double x, double lam
     // density: 1/2 pk G(a0 + k - 1) = 1/2 pk G_k (a0 + k) / y
     double dens = pk * g.G * (a0 + kd) * inv_y;
 
-    // forward j = k+1, k+2, ...
-    {
-        double p = pk, S = g.small, G = g.G;
-        for (long long j = k + 1; j < k + 100000; ++j) {
-            p *= h * t.rj(j);
-            // S_j from S_{j-1}: P decreases by G_{j-1}, Q increases by it
-            S = lower ? fmax(S - G, 0.0) : S + G;
-            dens += p * G;  // G_{j-1} = G(a0 + j - 1)
-            G *= y * t.raj(j);
-            wsum += p;
-            acc += p * S;
-            if (p < 1e-18 && static_cast<double>(j) > h) break;
-        }
-    }
-    // backward j = k-1, ..., 0
-    {
-        double p = pk, S = g.small, G = g.G;
-        for (long long j = k - 1; j >= 0; --j) {
-            const double jd = static_cast<double>(j);
-            p *= (jd + 1.0) * inv_h;
-            G *= (a0 + jd + 1.0) * inv_y;  // G_j = G_{j+1} (a0 + j + 1) / y
-            S = lower ? S + G : fmax(S - G, 0.0);
-            wsum += p;
-            acc += p * S;
-            dens += p * G * (a0 + jd) * inv_y;  // G_{j-1}
-            if (p < 1e-18) break;
-        }
+    if (lower) {
+        nc_forward<true>(t, k, kd, h, y, pk, g.small, g.G, wsum, acc, dens);
+        nc_backward<true>(a0, k, kd, inv_h, inv_y, pk, g.small, g.G, wsum, acc, dens);
+    } else {
+        nc_forward<false>(t, k, kd, h, y, pk, g.small, g.G, wsum, acc, dens);
+        nc_backward<false>(a0, k, kd, inv_h, inv_y, pk, g.small, g.G, wsum, acc, dens);
     }
     NcCdf r;
     const double side = acc / wsum;
