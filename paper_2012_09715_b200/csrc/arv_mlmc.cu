@@ -277,10 +277,10 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(L
                                                                  double *__restrict__ paths,
                                                                  unsigned long long *__restrict__ n_fail) {
     extern __shared__ double smd[];
-    const NcTables nct = nc_tables_init(smd, A.nu_exact);  // 4 * kNcTab doubles
+    const NcTables nct = nc_tables_init(smd, A.nu_exact);  // kNcSmemDoubles doubles
     const double *tab = stacks;
     if (use_smem) {
-        double *st = smd + 4 * kNcTab;
+        double *st = smd + kNcSmemDoubles;
         const int64_t total = 2 * n_knots * (DEG + 1) * K1;
         for (int64_t k = threadIdx.x; k < total; k += blockDim.x) st[k] = __ldg(stacks + k);
         __syncthreads();
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(256) k_ncchi2_cdf(const double *__restrict__ x
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const double li = nlam == 1 ? lam[0] : lam[i];
         const double xi = x[i];
-        out[i] = xi <= 0.0 ? 0.0 : ncchi2_cdf_minus(nct, xi, li, 0.0, 1.0).resid;
+        out[i] = xi <= 0.0 ? 0.0 : ncchi2_cdf_minus(nct, xi, li, 0.0).resid;
     }
 }
 
@@ -482,12 +482,12 @@ int arv_mlmc_cir_exact_level(const arv_level_spec *spec, const double *stacks, i
     double *parts = static_cast<double *>(workspace);
     const size_t bytes = sizeof(double) * 2 * n_knots * (degree + 1) * K1;
     const int use_smem = bytes <= 128 * 1024;
-    const size_t smem = sizeof(double) * 4 * kNcTab + (use_smem ? bytes : 0);
+    const size_t smem = sizeof(double) * kNcSmemDoubles + (use_smem ? bytes : 0);
     cudaStream_t s = as_stream(stream);
     unsigned long long *nf = reinterpret_cast<unsigned long long *>(n_fail);
 #define ARV_CASE(D)                                                                                          \
     case D:                                                                                                  \
-        if (smem > 48 * 1024)                                                                                \
+        if (smem > 40 * 1024)                                                                                \
             cudaFuncSetAttribute(k_cir_exact_level<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         k_cir_exact_level<D><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, stacks, n_knots, K1, use_smem, parts, paths, nf); \
         break;
@@ -510,7 +510,7 @@ int arv_ncchi2_inv_cdf(const double *u, const double *lam, int64_t nlam, double 
     if (!(nu > 0)) return set_error(ARV_ERR_DOMAIN, "degrees of freedom must be > 0");
     if (nlam != 1 && nlam != n) return set_error(ARV_ERR_CONFIG, "per-element lambda must match the shape of u");
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
-    const size_t smem = sizeof(double) * 4 * kNcTab;
+    const size_t smem = sizeof(double) * kNcSmemDoubles;
     k_ncchi2_inv<<<stream_grid(n, 256, 8), 256, smem, as_stream(stream)>>>(u, lam, nlam, nu, x0, out, resid, n);
     note_launch();
     return check_launch("arv_ncchi2_inv_cdf");
@@ -520,7 +520,7 @@ int arv_ncchi2_cdf(const double *x, const double *lam, int64_t nlam, double nu, 
     if (!(nu > 0)) return set_error(ARV_ERR_DOMAIN, "degrees of freedom must be > 0");
     if (nlam != 1 && nlam != n) return set_error(ARV_ERR_CONFIG, "per-element lambda must match the shape of x");
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
-    const size_t smem = sizeof(double) * 4 * kNcTab;
+    const size_t smem = sizeof(double) * kNcSmemDoubles;
     k_ncchi2_cdf<<<stream_grid(n, 256, 8), 256, smem, as_stream(stream)>>>(x, lam, nlam, nu, out, n);
     note_launch();
     return check_launch("arv_ncchi2_cdf");
