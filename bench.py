@@ -126,16 +126,19 @@ def cpu_port_rate(total: int, threads: int) -> tuple[float, float]:
 
     c = np.load(os.path.join(REPO, "paper_2012_09715_b200", "data", "tables.npz"))[TABLE].astype(np.float32)
     per = max(4, (total // threads) & ~3)
-    bufs = [np.empty(per, dtype=np.float32) for _ in range(threads)]
+    chunk = min(per, 1 << 22)  # bounded host memory; each thread writes its range chunk by chunk
+    bufs = [np.empty(chunk, dtype=np.float32) for _ in range(threads)]
     cptr = c.ctypes.data_as(oracle.oracle.C.c_void_p)
     vp = oracle.oracle.C.c_void_p
 
     def work(i):
         o = bufs[i].ctypes.data_as(vp)
-        if TABLE.startswith("constant"):
-            oracle.lib.orc_pcg32_constant_f32(42, 0, i * per, cptr, int(np.log2(c.size)), o, per)
-        else:
-            oracle.lib.orc_pcg32_subdyadic_f32(42, 0, i * per, cptr, 1, 16, 3, o, per)
+        for lo in range(0, per, chunk):
+            m = min(chunk, per - lo)
+            if TABLE.startswith("constant"):
+                oracle.lib.orc_pcg32_constant_f32(42, 0, i * per + lo, cptr, int(np.log2(c.size)), o, m)
+            else:
+                oracle.lib.orc_pcg32_subdyadic_f32(42, 0, i * per + lo, cptr, 1, 16, 3, o, m)
 
     with ThreadPoolExecutor(threads) as ex:
         t0 = time.perf_counter()
@@ -154,7 +157,7 @@ def cpu_threads() -> int:
 def cpu_baseline(target_seconds: float = 8.0) -> dict:
     threads = cpu_threads()
     r1, _ = cpu_port_rate(1 << 22, threads)  # calibration
-    total = int(min(max(r1 * target_seconds, 1 << 22), 1 << 31))
+    total = int(min(max(r1 * target_seconds, 1 << 22), 1 << 36))
     rate, dt = cpu_port_rate(total, threads)
     model = ""
     try:
