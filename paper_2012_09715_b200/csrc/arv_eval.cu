@@ -5,46 +5,142 @@
 #include "arv_common.cuh"
 #include "arv_eval_dev.cuh"
 
+#include <mutex>
+
 namespace arv {
 
 constexpr int kEvalBlock = 256;
 constexpr int kEvalPerSM = 8;
 
-static inline int eval_grid(int64_t n) { return stream_grid(n, kEvalBlock, kEvalPerSM); }
+// Grid = resident CTAs per SM (from the occupancy calculator, cached per
+// kernel and dynamic smem size) x SMs, so the grid-stride loop runs as one
+// wave whatever the kernel's register count; small n gets fewer CTAs.
+static int eval_grid(const void *fn, int64_t n, size_t smem) {
+    struct Entry {
+        const void *fn;
+        size_t smem;
+        int per_sm;
+    };
+    static Entry cache[64];
+    static int used = 0;
+    static std::mutex mu;
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        for (int i = 0; i < used; ++i)
+            if (cache[i].fn == fn && cache[i].smem == smem) per_sm = cache[i].per_sm;
+    }
+    if (per_sm == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kEvalBlock, smem) != cudaSuccess ||
+            per_sm < 1) {
+            (void)cudaGetLastError();
+            per_sm = 1;
+        }
+        per_sm = per_sm < kEvalPerSM ? per_sm : kEvalPerSM;
+        std::lock_guard<std::mutex> lock(mu);
+        if (used < 64) cache[used++] = {fn, smem, per_sm};
+    }
+    return stream_grid(n, kEvalBlock, per_sm);
+}
 
-#define ARV_GRID_STRIDE(i, n)                                                               \
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n); \
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+
+// Element-wise map out[i] = f(u[i] [, aux[i]]).  When every pointer is
+// 16-byte aligned the body moves 16-byte vectors, two per thread in flight
+// (a scalar 4-byte stream keeps ~1 MB in flight chip-wide, far below the
+// ~6 MB the HBM latency-bandwidth product asks for); the remainder and
+// misaligned views take the scalar grid-stride loop.  Streaming cache hints
+// on both sides: every byte is touched once.
+template <typename In, typename Out, int V, typename F, typename... A>
+__device__ __forceinline__ void ew_apply(const uint4 &r, const uint4 *ra, Out *dst, F &f) {
+    In a[V];
+    memcpy(a, &r, 16);
+    Out b[V];
+    if constexpr (sizeof...(A) == 0) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) b[k] = f(a[k]);
+    } else {
+        In x[V];
+        memcpy(x, ra, 16);
+#pragma unroll
+        for (int k = 0; k < V; ++k) b[k] = f(a[k], x[k]);
+    }
+    constexpr int VO = static_cast<int>(sizeof(b) / 16);
+#pragma unroll
+    for (int k = 0; k < VO; ++k) {
+        uint4 w;
+        memcpy(&w, reinterpret_cast<const char *>(b) + 16 * k, 16);
+        __stcs(reinterpret_cast<uint4 *>(dst) + k, w);
+    }
+}
+
+template <bool AUX, typename In, typename Out, typename F>
+__device__ __forceinline__ void ew_map(const In *__restrict__ u, const In *__restrict__ aux, Out *__restrict__ out,
+                                       int64_t n, F f) {
+    constexpr int V = 16 / sizeof(In);
+    static_assert(sizeof(Out) >= sizeof(In), "output vectors are whole 16-byte stores");
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    uintptr_t align = reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(out);
+    if (AUX) align |= reinterpret_cast<uintptr_t>(aux);
+    int64_t head = 0;
+    if ((align & 15) == 0) {
+        const int64_t nv = n / V;
+        const uint4 *uv = reinterpret_cast<const uint4 *>(u);
+        const uint4 *xv = reinterpret_cast<const uint4 *>(aux);
+        for (int64_t i = tid; i < nv; i += 2 * stride) {
+            const bool two = i + stride < nv;
+            const uint4 ra = __ldcs(uv + i);
+            uint4 rb = ra, xa, xb;
+            if (two) rb = __ldcs(uv + i + stride);
+            if (AUX) {
+                xa = __ldcs(xv + i);
+                xb = two ? __ldcs(xv + i + stride) : xa;
+            }
+            if constexpr (AUX) {
+                ew_apply<In, Out, V, F, In>(ra, &xa, out + i * V, f);
+                if (two) ew_apply<In, Out, V, F, In>(rb, &xb, out + (i + stride) * V, f);
+            } else {
+                ew_apply<In, Out, V, F>(ra, nullptr, out + i * V, f);
+                if (two) ew_apply<In, Out, V, F>(rb, nullptr, out + (i + stride) * V, f);
+            }
+        }
+        head = nv * V;
+    }
+    for (int64_t i = head + tid; i < n; i += stride) {
+        if constexpr (AUX) __stcs(out + i, f(__ldcs(u + i), __ldcs(aux + i)));
+        else __stcs(out + i, f(__ldcs(u + i)));
+    }
+}
 
 // ------------------------------------------------------- constant_eval --
 // _kernels.pyx:16-23: idx = (long long)(nvals * u), idx = min(idx, nvals-1).
-__global__ void __launch_bounds__(kEvalBlock) k_constant_eval(const double *__restrict__ values, int64_t nvals,
+__global__ void __launch_bounds__(kEvalBlock, 6) k_constant_eval(const double *__restrict__ values, int64_t nvals,
                                                               int use_smem, const double *__restrict__ u,
                                                               double *__restrict__ out, int64_t n) {
     extern __shared__ double smd[];
-    const double *tab = values;
-    if (use_smem) {
+    const double scale = static_cast<double>(nvals);
+    auto index = [=](double ui) {
+        long long idx = static_cast<long long>(__dmul_rn(scale, ui));
+        idx = idx < nvals ? idx : nvals - 1;
+        return idx < 0 ? 0 : idx;  // memory-safety clamp (u outside the (0,1) contract)
+    };
+    if (use_smem) {  // separate bodies so the staged table is read with LDS, not generic loads
         for (int i = threadIdx.x; i < nvals; i += blockDim.x) smd[i] = __ldg(values + i);
         __syncthreads();
-        tab = smd;
-    }
-    const double scale = static_cast<double>(nvals);
-    ARV_GRID_STRIDE(i, n) {
-        long long idx = static_cast<long long>(__dmul_rn(scale, __ldcs(u + i)));
-        idx = idx < nvals ? idx : nvals - 1;
-        idx = idx < 0 ? 0 : idx;  // memory-safety clamp (u outside the (0,1) contract)
-        __stcs(out + i, tab[idx]);
+        ew_map<false>(u, u, out, n, [=](double ui) { return smd[index(ui)]; });
+    } else {
+        ew_map<false>(u, u, out, n, [=](double ui) { return __ldg(values + index(ui)); });
     }
 }
 
 // -------------------------------------------------------- dyadic_index --
-__global__ void __launch_bounds__(kEvalBlock) k_dyadic_index(const double *__restrict__ u, int64_t cap,
+__global__ void __launch_bounds__(kEvalBlock, kEvalPerSM) k_dyadic_index(const double *__restrict__ u, int64_t cap,
                                                              long long *__restrict__ out, int64_t n) {
-    ARV_GRID_STRIDE(i, n) __stcs(out + i, dyadic_idx64(__ldcs(u + i), cap));
+    ew_map<false>(u, u, out, n, [=](double ui) { return dyadic_idx64(ui, cap); });
 }
 __global__ void __launch_bounds__(kEvalBlock) k_dyadic_index32(const float *__restrict__ u, int64_t cap,
                                                                long long *__restrict__ out, int64_t n) {
-    ARV_GRID_STRIDE(i, n) __stcs(out + i, dyadic_idx32(__ldcs(u + i), cap));
+    ew_map<false>(u, u, out, n, [=](float ui) { return dyadic_idx32(ui, cap); });
 }
 
 // --------------------------------------------------------- dyadic_eval --
@@ -58,8 +154,7 @@ __global__ void __launch_bounds__(kEvalBlock) k_dyadic_eval(const double *__rest
     for (int i = threadIdx.x; i < (DEG + 1) * K1; i += blockDim.x) smd[i] = __ldg(coeffs + i);
     __syncthreads();
     const long long cap = K1 - 1;
-    ARV_GRID_STRIDE(i, n) {
-        const double ui = __ldcs(u + i);
+    ew_map<false>(u, u, out, n, [=](double ui) {
         const bool pred = ui < 0.5;
         const double v = pred ? ui : __dsub_rn(1.0, ui);
         long long idx = dyadic_idx64(v, cap);
@@ -67,8 +162,8 @@ __global__ void __launch_bounds__(kEvalBlock) k_dyadic_eval(const double *__rest
         double z = smd[DEG * K1 + idx];
 #pragma unroll
         for (int d = DEG - 1; d >= 0; --d) z = __dadd_rn(__dmul_rn(z, v), smd[d * K1 + idx]);
-        __stcs(out + i, pred ? z : -z);
-    }
+        return pred ? z : -z;
+    });
 }
 
 template <int DEG>
@@ -79,8 +174,7 @@ __global__ void __launch_bounds__(kEvalBlock) k_dyadic_eval32(const float *__res
     for (int i = threadIdx.x; i < (DEG + 1) * K1; i += blockDim.x) smf[i] = __ldg(coeffs + i);
     __syncthreads();
     const long long cap = K1 - 1;
-    ARV_GRID_STRIDE(i, n) {
-        const float ui = __ldcs(u + i);
+    ew_map<false>(u, u, out, n, [=](float ui) {
         const bool pred = ui < 0.5f;
         const float v = pred ? ui : __fsub_rn(1.0f, ui);
         long long idx = dyadic_idx32(v, cap);
@@ -88,8 +182,8 @@ __global__ void __launch_bounds__(kEvalBlock) k_dyadic_eval32(const float *__res
         float z = smf[DEG * K1 + idx];
 #pragma unroll
         for (int d = DEG - 1; d >= 0; --d) z = __fadd_rn(__fmul_rn(z, v), smf[d * K1 + idx]);
-        __stcs(out + i, pred ? z : -z);
-    }
+        return pred ? z : -z;
+    });
 }
 
 // --------------------------------------------- octave x sub-interval f32 --
@@ -109,8 +203,7 @@ __global__ void __launch_bounds__(kEvalBlock) k_subdyadic_eval32(const float *__
     }
     __syncthreads();
     const int shift = 23 - b, base = (126 - K) << b;
-    ARV_GRID_STRIDE(i, n) {
-        const float ui = __ldcs(u + i);
+    ew_map<false>(u, u, out, n, [=](float ui) {
         const bool pred = ui < 0.5f;
         const float v = pred ? ui : __fsub_rn(1.0f, ui);
         int e = static_cast<int>(__float_as_uint(v) >> shift) - base;
@@ -118,8 +211,8 @@ __global__ void __launch_bounds__(kEvalBlock) k_subdyadic_eval32(const float *__
         float z = smf[DEG * plane + e];
 #pragma unroll
         for (int d = DEG - 1; d >= 0; --d) z = __fadd_rn(__fmul_rn(z, v), smf[d * plane + e]);
-        __stcs(out + i, pred ? z : -z);
-    }
+        return pred ? z : -z;
+    });
 }
 
 // --------------------------------------------------------- ncchi2_eval --
@@ -127,33 +220,44 @@ __global__ void __launch_bounds__(kEvalBlock) k_subdyadic_eval32(const float *__
 // lower at 1; knot bracketing j = min(floor(sqrt(nu/(lam+nu)) (n_knots-1)),
 // n_knots-2), linear interpolation in t.  All IEEE (div/sqrt round-to-nearest).
 template <int DEG>
+__device__ __forceinline__ void ncchi2_map(const double *tab, int64_t n_knots, int64_t K1, double nu,
+                                           const double *__restrict__ u, const double *__restrict__ lam, int64_t nlam,
+                                           double *__restrict__ out, int64_t n) {
+    if (nlam == 1) {  // shared lambda: knot bracket (two sqrt, one div) once per thread
+        const NcKnot kn = ncchi2_knot(n_knots, nu, __ldg(lam));
+        ew_map<false>(u, u, out, n, [=](double ui) { return ncchi2_eval_at<DEG>(tab, n_knots, K1, kn, ui); });
+    } else {
+        ew_map<true>(u, lam, out, n, [=](double ui, double li) {
+            return ncchi2_eval_at<DEG>(tab, n_knots, K1, ncchi2_knot(n_knots, nu, li), ui);
+        });
+    }
+}
+
+template <int DEG>
 __global__ void __launch_bounds__(kEvalBlock) k_ncchi2_eval(const double *__restrict__ stacks, int64_t n_knots,
                                                             int64_t K1, int use_smem, double nu,
                                                             const double *__restrict__ u,
                                                             const double *__restrict__ lam, int64_t nlam,
                                                             double *__restrict__ out, int64_t n) {
     extern __shared__ double smd[];
-    const double *tab = stacks;
     if (use_smem) {
         const int64_t total = 2 * n_knots * (DEG + 1) * K1;
         for (int64_t i = threadIdx.x; i < total; i += blockDim.x) smd[i] = __ldg(stacks + i);
         __syncthreads();
-        tab = smd;
-    }
-    ARV_GRID_STRIDE(i, n) {
-        const double li = nlam == 1 ? __ldg(lam) : __ldcs(lam + i);
-        __stcs(out + i, ncchi2_eval1<DEG>(tab, n_knots, K1, nu, __ldcs(u + i), li));
+        ncchi2_map<DEG>(smd, n_knots, K1, nu, u, lam, nlam, out, n);
+    } else {
+        ncchi2_map<DEG>(stacks, n_knots, K1, nu, u, lam, nlam, out, n);
     }
 }
 
 // ---------------------------------------------------------- AS241 exact --
 __global__ void __launch_bounds__(kEvalBlock) k_gauss_inv_cdf(const double *__restrict__ u, double *__restrict__ out,
                                                               int64_t n) {
-    ARV_GRID_STRIDE(i, n) __stcs(out + i, as241_f64(__ldcs(u + i)));
+    ew_map<false>(u, u, out, n, [](double ui) { return as241_f64(ui); });
 }
 __global__ void __launch_bounds__(kEvalBlock) k_gauss_inv_cdf32(const float *__restrict__ u, float *__restrict__ out,
                                                                 int64_t n) {
-    ARV_GRID_STRIDE(i, n) __stcs(out + i, as241_f32(__ldcs(u + i)));
+    ew_map<false>(u, u, out, n, [](float ui) { return as241_f32(ui); });
 }
 
 static int finish(const char *what) {
@@ -180,19 +284,19 @@ int arv_constant_eval(const double *values, int64_t nvals, const double *u, doub
     const int use_smem = nvals <= 8192;  // 64 KiB
     const size_t smem = use_smem ? sizeof(double) * nvals : 0;
     if (int rc = set_smem((const void *)k_constant_eval, smem)) return rc;
-    k_constant_eval<<<eval_grid(n), kEvalBlock, smem, as_stream(stream)>>>(values, nvals, use_smem, u, out, n);
+    k_constant_eval<<<eval_grid((const void *)k_constant_eval, n, smem), kEvalBlock, smem, as_stream(stream)>>>(values, nvals, use_smem, u, out, n);
     return finish("arv_constant_eval");
 }
 
 int arv_dyadic_index(const double *u, int64_t n, int64_t cap, int64_t *out, void *stream) {
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
-    k_dyadic_index<<<eval_grid(n), kEvalBlock, 0, as_stream(stream)>>>(u, cap, reinterpret_cast<long long *>(out), n);
+    k_dyadic_index<<<eval_grid((const void *)k_dyadic_index, n, 0), kEvalBlock, 0, as_stream(stream)>>>(u, cap, reinterpret_cast<long long *>(out), n);
     return finish("arv_dyadic_index");
 }
 
 int arv_dyadic_index32(const float *u, int64_t n, int64_t cap, int64_t *out, void *stream) {
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
-    k_dyadic_index32<<<eval_grid(n), kEvalBlock, 0, as_stream(stream)>>>(u, cap, reinterpret_cast<long long *>(out), n);
+    k_dyadic_index32<<<eval_grid((const void *)k_dyadic_index32, n, 0), kEvalBlock, 0, as_stream(stream)>>>(u, cap, reinterpret_cast<long long *>(out), n);
     return finish("arv_dyadic_index32");
 }
 
@@ -207,12 +311,11 @@ int arv_dyadic_eval(const double *coeffs, int degree, int64_t K1, const double *
     if (K1 < 2 || K1 > 4096) return set_error(ARV_ERR_CONFIG, "dyadic_eval: bad interval count %lld", (long long)K1);
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
     const size_t smem = sizeof(double) * (degree + 1) * K1;
-    const int grid = eval_grid(n);
     cudaStream_t s = as_stream(stream);
 #define ARV_CASE(D)                                                                     \
     case D:                                                                             \
         if (int rc = set_smem((const void *)k_dyadic_eval<D>, smem)) return rc;          \
-        k_dyadic_eval<D><<<grid, kEvalBlock, smem, s>>>(coeffs, K1, u, out, n);          \
+        k_dyadic_eval<D><<<eval_grid((const void *)k_dyadic_eval<D>, n, smem), kEvalBlock, smem, s>>>(coeffs, K1, u, out, n);          \
         break;
     ARV_DEG_SWITCH(degree, ARV_CASE)
 #undef ARV_CASE
@@ -224,12 +327,11 @@ int arv_dyadic_eval32(const float *coeffs, int degree, int64_t K1, const float *
     if (K1 < 2 || K1 > 4096) return set_error(ARV_ERR_CONFIG, "dyadic_eval32: bad interval count %lld", (long long)K1);
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
     const size_t smem = sizeof(float) * (degree + 1) * K1;
-    const int grid = eval_grid(n);
     cudaStream_t s = as_stream(stream);
 #define ARV_CASE(D)                                                                     \
     case D:                                                                             \
         if (int rc = set_smem((const void *)k_dyadic_eval32<D>, smem)) return rc;        \
-        k_dyadic_eval32<D><<<grid, kEvalBlock, smem, s>>>(coeffs, K1, u, out, n);        \
+        k_dyadic_eval32<D><<<eval_grid((const void *)k_dyadic_eval32<D>, n, smem), kEvalBlock, smem, s>>>(coeffs, K1, u, out, n);        \
         break;
     ARV_DEG_SWITCH(degree, ARV_CASE)
 #undef ARV_CASE
@@ -242,11 +344,10 @@ int arv_subdyadic_eval32(const float *coeffs, int degree, int K, int sub_bits, c
     if (sub_bits < 0 || sub_bits > 5) return set_error(ARV_ERR_CONFIG, "sub_bits must be in [0, 5], got %d", sub_bits);
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
     const size_t smem = sizeof(float) * (degree + 1) * ((size_t)(K + 1) << sub_bits);
-    const int grid = eval_grid(n);
     cudaStream_t s = as_stream(stream);
 #define ARV_CASE(D)                                                                       \
     case D:                                                                               \
-        k_subdyadic_eval32<D><<<grid, kEvalBlock, smem, s>>>(coeffs, K, sub_bits, u, out, n); \
+        k_subdyadic_eval32<D><<<eval_grid((const void *)k_subdyadic_eval32<D>, n, smem), kEvalBlock, smem, s>>>(coeffs, K, sub_bits, u, out, n); \
         break;
     ARV_DEG_SWITCH(degree, ARV_CASE)
 #undef ARV_CASE
@@ -262,12 +363,11 @@ int arv_ncchi2_eval(const double *stacks, int64_t n_knots, int degree, int64_t K
     const size_t bytes = sizeof(double) * 2 * n_knots * (degree + 1) * K1;
     const int use_smem = bytes <= 160 * 1024;
     const size_t smem = use_smem ? bytes : 0;
-    const int grid = eval_grid(n);
     cudaStream_t s = as_stream(stream);
 #define ARV_CASE(D)                                                                                       \
     case D:                                                                                               \
         if (int rc = set_smem((const void *)k_ncchi2_eval<D>, smem)) return rc;                            \
-        k_ncchi2_eval<D><<<grid, kEvalBlock, smem, s>>>(stacks, n_knots, K1, use_smem, nu, u, lam, nlam, out, n); \
+        k_ncchi2_eval<D><<<eval_grid((const void *)k_ncchi2_eval<D>, n, smem), kEvalBlock, smem, s>>>(stacks, n_knots, K1, use_smem, nu, u, lam, nlam, out, n); \
         break;
     ARV_DEG_SWITCH(degree, ARV_CASE)
 #undef ARV_CASE
@@ -276,13 +376,13 @@ int arv_ncchi2_eval(const double *stacks, int64_t n_knots, int degree, int64_t K
 
 int arv_gaussian_inv_cdf(const double *u, double *out, int64_t n, void *stream) {
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
-    k_gauss_inv_cdf<<<eval_grid(n), kEvalBlock, 0, as_stream(stream)>>>(u, out, n);
+    k_gauss_inv_cdf<<<eval_grid((const void *)k_gauss_inv_cdf, n, 0), kEvalBlock, 0, as_stream(stream)>>>(u, out, n);
     return finish("arv_gaussian_inv_cdf");
 }
 
 int arv_gaussian_inv_cdf32(const float *u, float *out, int64_t n, void *stream) {
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
-    k_gauss_inv_cdf32<<<eval_grid(n), kEvalBlock, 0, as_stream(stream)>>>(u, out, n);
+    k_gauss_inv_cdf32<<<eval_grid((const void *)k_gauss_inv_cdf32, n, 0), kEvalBlock, 0, as_stream(stream)>>>(u, out, n);
     return finish("arv_gaussian_inv_cdf32");
 }
 

@@ -37,24 +37,37 @@ __device__ __forceinline__ double gauss_table_eval(const double *c, int64_t K1, 
 // upper half at 0, lower at 1; knot bracketing j = min(floor(sqrt(nu /
 // (lam + nu)) (n_knots - 1)), n_knots - 2); linear interpolation in t.
 // All IEEE (div / sqrt round-to-nearest), separately rounded mul/add.
-template <int DEG>
-__device__ __forceinline__ double ncchi2_eval1(const double *tab, int64_t n_knots, int64_t K1, double nu, double ui,
-                                               double lam_i) {
-    const long long cap = K1 - 1;
-    const double shift = __dadd_rn(lam_i, nu);
-    const double scale2 = __dmul_rn(2.0, __dsqrt_rn(shift));
-    const double s = __dsqrt_rn(__ddiv_rn(nu, shift));
+// The lambda-dependent half (shift, scale, knot bracket) is split out so a
+// batch with one shared lambda computes it once per thread: the two IEEE
+// square roots and the division dominate the per-element FP64 cost.
+struct NcKnot {
+    double shift, scale2, t;
+    long long j;
+};
+
+__device__ __forceinline__ NcKnot ncchi2_knot(int64_t n_knots, double nu, double lam_i) {
+    NcKnot k;
+    k.shift = __dadd_rn(lam_i, nu);
+    k.scale2 = __dmul_rn(2.0, __dsqrt_rn(k.shift));
+    const double s = __dsqrt_rn(__ddiv_rn(nu, k.shift));
     const double g = __dmul_rn(s, static_cast<double>(n_knots - 1));
     long long j = static_cast<long long>(g);
     j = j < n_knots - 2 ? j : n_knots - 2;
-    j = j < 0 ? 0 : j;
-    const double t = __dsub_rn(g, static_cast<double>(j));
+    k.j = j < 0 ? 0 : j;
+    k.t = __dsub_rn(g, static_cast<double>(k.j));
+    return k;
+}
+
+template <int DEG>
+__device__ __forceinline__ double ncchi2_eval_at(const double *tab, int64_t n_knots, int64_t K1, const NcKnot &k,
+                                                 double ui) {
+    const long long cap = K1 - 1;
     const long long sel = ui < 0.5 ? 1 : 0;
     const double v = sel ? ui : __dsub_rn(1.0, ui);
     long long idx = dyadic_idx64(v, cap);
     idx = idx < 0 ? 0 : idx;
     const int64_t knot = (DEG + 1) * K1;
-    const double *t0 = tab + (sel * n_knots + j) * knot;
+    const double *t0 = tab + (sel * n_knots + k.j) * knot;
     const double *t1 = t0 + knot;
     double z0 = t0[DEG * K1 + idx];
     double z1 = t1[DEG * K1 + idx];
@@ -63,7 +76,13 @@ __device__ __forceinline__ double ncchi2_eval1(const double *tab, int64_t n_knot
         z0 = __dadd_rn(__dmul_rn(z0, v), t0[d * K1 + idx]);
         z1 = __dadd_rn(__dmul_rn(z1, v), t1[d * K1 + idx]);
     }
-    return __dadd_rn(shift, __dmul_rn(scale2, __dadd_rn(z0, __dmul_rn(t, __dsub_rn(z1, z0)))));
+    return __dadd_rn(k.shift, __dmul_rn(k.scale2, __dadd_rn(z0, __dmul_rn(k.t, __dsub_rn(z1, z0)))));
+}
+
+template <int DEG>
+__device__ __forceinline__ double ncchi2_eval1(const double *tab, int64_t n_knots, int64_t K1, double nu, double ui,
+                                               double lam_i) {
+    return ncchi2_eval_at<DEG>(tab, n_knots, K1, ncchi2_knot(n_knots, nu, lam_i), ui);
 }
 
 }  // namespace arv

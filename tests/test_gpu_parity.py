@@ -268,6 +268,65 @@ class TestDropInKernels:
         k.ncchi2_eval(tables_npz["ncchi2_cir_k64_stacks"], 2.0, bad, np.array([1.0]), out)
         torch.cuda.synchronize()
 
+    @pytest.mark.parametrize("n", [1, 2, 3, 5, 17, 1000, 4099, 70001])
+    @pytest.mark.parametrize("pad_in,pad_out", [(0, 0), (1, 0), (0, 1), (2, 3)])
+    def test_device_views_ragged(self, arv, orc, tables_npz, n, pad_in, pad_out):
+        """Device-resident inputs at every alignment: 16-byte vector body plus
+        scalar tail when the views are aligned, scalar grid-stride otherwise."""
+        k = arv.get_kernels()
+        rng = np.random.default_rng(n * 7 + pad_in)
+        u = rng.random(n)
+        lam = rng.random(n) * 300.0
+        ud = torch.zeros(n + 8, dtype=torch.float64, device="cuda")
+        ud[pad_in:pad_in + n] = torch.from_numpy(u).cuda()
+        ld = torch.zeros(n + 8, dtype=torch.float64, device="cuda")
+        ld[pad_in:pad_in + n] = torch.from_numpy(lam).cuda()
+        uv, lv = ud[pad_in:pad_in + n], ld[pad_in:pad_in + n]
+        o = torch.full((n + 8,), float("nan"), dtype=torch.float64, device="cuda")
+        ov = o[pad_out:pad_out + n]
+
+        def check(got, ref):
+            assert np.array_equal(bits(got.cpu().numpy()), bits(np.asarray(ref)))
+            assert torch.isnan(o[:pad_out]).all() and torch.isnan(o[pad_out + n:]).all()
+
+        lin = tables_npz["dyadic_linear_k15"]
+        k.dyadic_eval(lin, uv, ov)
+        check(ov, orc.dyadic_eval(lin, u))
+        cv = tables_npz["constant_q10_l1"]
+        k.constant_eval(cv, uv, ov)
+        check(ov, orc.constant_eval(cv, u))
+        st, nu = tables_npz["ncchi2_cir_k64_stacks"], float(tables_npz["ncchi2_cir_k64_nu"])
+        k.ncchi2_eval(st, nu, uv, lv, ov)
+        check(ov, orc.ncchi2_eval(st, nu, u, lam))
+        k.ncchi2_eval(st, nu, uv, torch.tensor([7.5], dtype=torch.float64, device="cuda"), ov)
+        check(ov, orc.ncchi2_eval(st, nu, u, np.array([7.5])))
+        k.gaussian_inv_cdf(uv, ov)  # tails go through log / sqrt: libm-level agreement
+        got, ref = ov.cpu().numpy(), orc.as241_f64(u)
+        central = np.abs(u - 0.5) <= 0.425
+        assert np.array_equal(bits(got[central]), bits(ref[central]))
+        np.testing.assert_allclose(got, ref, rtol=4e-16 * 8, atol=0)
+        idx = k.dyadic_index(uv, 15)
+        assert np.array_equal(idx.cpu().numpy(), orc.dyadic_index(u, 15))
+
+        u32 = u.astype(np.float32)
+        u32 = np.where(u32 >= 1.0, np.float32(0.5), u32)
+        u32d = torch.zeros(n + 8, dtype=torch.float32, device="cuda")
+        u32d[pad_in:pad_in + n] = torch.from_numpy(u32).cuda()
+        u32v = u32d[pad_in:pad_in + n]
+        o = torch.full((n + 8,), float("nan"), dtype=torch.float32, device="cuda")
+        ov = o[pad_out:pad_out + n]
+        k.dyadic_eval32(lin.astype(np.float32), u32v, ov)
+        check(ov, orc.dyadic_eval32(lin.astype(np.float32), u32))
+        c = tables_npz["subdyadic_linear_k16_s8"].astype(np.float32)
+        k.subdyadic_eval32(c, 3, u32v, ov)
+        check(ov, orc.subdyadic_eval32(c, 3, u32))
+        k.gaussian_inv_cdf32(u32v, ov)
+        got32 = ov.cpu().numpy()  # f32 rational after device vs glibc logf / sqrtf: a few ulp
+        ulp = np.abs(bits(got32).astype(np.int64) - bits(orc.as241_f32(u32)).astype(np.int64))
+        assert ulp.max() <= 8
+        np.testing.assert_allclose(got32, orc.as241_f64(u32.astype(np.float64)), rtol=2e-6, atol=2e-6)
+        assert np.array_equal(k.dyadic_index32(u32v, 15).cpu().numpy(), orc.dyadic_index32(u32, 15))
+
     def test_launch_counter_advances(self, arv):
         from paper_2012_09715_b200 import _native
 
