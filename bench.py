@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import sys
@@ -360,8 +361,9 @@ def run_ours(args) -> None:
     value = world * n * args.steps / t_max
     per_launch = t_max / args.steps
 
-    # parity spot check of this rank's last output against AS241 error bound (cheap, untimed)
-    ok = bool(torch.isfinite(out[:1 << 20]).all())
+    # approximation quality of this step's output (untimed): error against the
+    # exact AS241 f64 quantile of the same uniforms, over every sample
+    quality = approximation_error(arv, out, offset)
 
     # e2e: the public API with a pinned host buffer, D2H inside the timed region
     host = torch.empty(n, dtype=torch.float32, pin_memory=True)
@@ -422,7 +424,7 @@ def run_ours(args) -> None:
                 "path": "Pcg32Stream.sample_host -> pinned host buffer, chunked D2H overlapped with generation"},
         "gpu_launches": int(launches),
         "clocks": sampler.summary(),
-        "finite_check": ok,
+        "quality": quality,
     }
     if mlmc is not None:
         line["mlmc"] = mlmc
@@ -431,6 +433,23 @@ def run_ours(args) -> None:
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def approximation_error(arv, out, offset: int, chunk: int = 1 << 26) -> dict:
+    """RMSE / max |error| of the f32 table samples against AS241 in f64 on the
+    same PCG32 uniforms, all samples of one step."""
+    import torch
+
+    n = out.numel()
+    sq, mx = 0.0, 0.0
+    for lo in range(0, n, chunk):
+        m = min(chunk, n - lo)
+        ex = arv.Pcg32Stream(42, 0, counter=offset + lo).sample_exact64(m)
+        d = out[lo:lo + m].double() - ex
+        sq += float(torch.dot(d, d))
+        mx = max(mx, float(d.abs().max()))
+    return {"rmse_vs_as241_f64": math.sqrt(sq / n), "max_abs_err": mx, "samples": n,
+            "note": "table approximation error, not a parity measure (parity is bit-exact, tests/)"}
 
 
 def mlmc_metrics(arv, args, rank, world, device) -> dict:
