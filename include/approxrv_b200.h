@@ -130,7 +130,8 @@ ARV_API int arv_store_probe_ex(float *out, int64_t n, int mode, void *stream);
 
 /* Launch-shape knobs of the fused generators (process-wide):
  * ARV_TUNE_GROUP = samples per thread-group, 4 (v4 stores) or 8 (v8, default);
- * ARV_TUNE_CTAS_PER_SM = resident 256-thread CTAs per SM (default 8). */
+ * ARV_TUNE_CTAS_PER_SM = 256-thread CTAs per SM; 0 (default) = auto: the
+ * kernel's resident count, fewer when n is small (>= 64 samples per thread). */
 #define ARV_TUNE_GROUP 1
 #define ARV_TUNE_CTAS_PER_SM 2
 ARV_API int arv_set_tuning(int key, int value);

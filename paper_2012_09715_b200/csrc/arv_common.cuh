@@ -21,6 +21,9 @@ int set_error(int code, const char *fmt, ...);
 int check_launch(const char *what);
 void note_launch(int n = 1);
 int device_sm_count();
+// Resident CTAs per SM of `fn` at this block size and dynamic smem (occupancy
+// calculator, cached per kernel / shape / device).
+int resident_ctas(const void *fn, int block, size_t smem);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -5,7 +5,6 @@
 #include "arv_common.cuh"
 #include "arv_eval_dev.cuh"
 
-#include <mutex>
 
 namespace arv {
 
@@ -16,31 +15,8 @@ constexpr int kEvalPerSM = 8;
 // kernel and dynamic smem size) x SMs, so the grid-stride loop runs as one
 // wave whatever the kernel's register count; small n gets fewer CTAs.
 static int eval_grid(const void *fn, int64_t n, size_t smem) {
-    struct Entry {
-        const void *fn;
-        size_t smem;
-        int per_sm;
-    };
-    static Entry cache[64];
-    static int used = 0;
-    static std::mutex mu;
-    int per_sm = 0;
-    {
-        std::lock_guard<std::mutex> lock(mu);
-        for (int i = 0; i < used; ++i)
-            if (cache[i].fn == fn && cache[i].smem == smem) per_sm = cache[i].per_sm;
-    }
-    if (per_sm == 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kEvalBlock, smem) != cudaSuccess ||
-            per_sm < 1) {
-            (void)cudaGetLastError();
-            per_sm = 1;
-        }
-        per_sm = per_sm < kEvalPerSM ? per_sm : kEvalPerSM;
-        std::lock_guard<std::mutex> lock(mu);
-        if (used < 64) cache[used++] = {fn, smem, per_sm};
-    }
-    return stream_grid(n, kEvalBlock, per_sm);
+    const int per_sm = resident_ctas(fn, kEvalBlock, smem);
+    return stream_grid(n, kEvalBlock, per_sm < kEvalPerSM ? per_sm : kEvalPerSM);
 }
 
 

@@ -2,6 +2,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <mutex>
 
 #include "arv_common.cuh"
 
@@ -32,6 +33,34 @@ int device_sm_count() {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
         return sms;
     return kNumSMs;
+}
+
+int resident_ctas(const void *fn, int block, size_t smem) {
+    struct Entry {
+        const void *fn;
+        int block, dev;
+        size_t smem;
+        int ctas;
+    };
+    static Entry cache[128];
+    static int used = 0;
+    static std::mutex mu;
+    int dev = 0;
+    (void)cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        for (int i = 0; i < used; ++i)
+            if (cache[i].fn == fn && cache[i].block == block && cache[i].smem == smem && cache[i].dev == dev)
+                return cache[i].ctas;
+    }
+    int ctas = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, fn, block, smem) != cudaSuccess || ctas < 1) {
+        (void)cudaGetLastError();
+        ctas = 1;
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    if (used < 128) cache[used++] = {fn, block, dev, smem, ctas};
+    return ctas;
 }
 
 }  // namespace arv

@@ -34,7 +34,7 @@ namespace arv {
 constexpr int kGenUnroll = ARV_GEN_UNROLL;
 // Process-wide launch shape knobs (arv_set_tuning); defaults from sweeps.
 static int g_group = 8;        // samples per thread-group: 4 (v4) or 8 (v8)
-static int g_ctas_per_sm = 8;  // resident CTAs per SM (256 threads each)
+static int g_ctas_per_sm = 0;  // CTAs per SM (256 threads each); 0 = auto (see gen_grid)
 
 constexpr int kJumpBits = 24;  // grid threads < 2^24
 
@@ -371,8 +371,20 @@ static int store_mode(const void *out) {
     return 1;
 }
 
-static int gen_grid(int64_t n, int mode) {
-    return stream_grid((n + mode - 1) / mode, kGenBlock, g_ctas_per_sm);
+// One wave: CTAs per SM = the kernel's resident count (a second partial wave
+// of a grid-stride kernel costs 2-7% at 2^28, tools/sweep_launch.py), fewer
+// for small n so that every thread keeps >= kMinPerThread samples to amortise
+// its jump-ahead (2^24: 4 CTAs/SM beat 8 by 7%; 2^20: 1-2 beat 8 by 30%).
+constexpr int64_t kMinPerThread = 64;
+
+static int gen_grid(const void *fn, int64_t n, int mode, size_t smem = 0) {
+    int per_sm = g_ctas_per_sm;
+    if (per_sm <= 0) {
+        const int64_t want = n / (static_cast<int64_t>(device_sm_count()) * kGenBlock * kMinPerThread);
+        const int occ = resident_ctas(fn, kGenBlock, smem);
+        per_sm = static_cast<int>(want < 1 ? 1 : (want < occ ? want : occ));
+    }
+    return stream_grid((n + mode - 1) / mode, kGenBlock, per_sm);
 }
 
 template <class Eval>
@@ -381,7 +393,10 @@ static int launch_simple(uint64_t seed, uint64_t sid, uint64_t offset, uint32_t 
     if (n < 0) return set_error(ARV_ERR_CONFIG, "%s: negative n", what);
     if (n == 0) return ARV_OK;
     const int mode = store_mode(out);
-    const int grid = gen_grid(n, mode);
+    const void *fn = mode == 8   ? (const void *)k_gen_simple<8, Eval>
+                     : mode == 4 ? (const void *)k_gen_simple<4, Eval>
+                                 : (const void *)k_gen_simple<1, Eval>;
+    const int grid = gen_grid(fn, n, mode);
     const int64_t T = static_cast<int64_t>(grid) * kGenBlock;
     const GenArgs a = make_gen_args(seed, sid, offset, n, T, mode == 1 ? 4 : mode);
     cudaStream_t s = as_stream(stream);
@@ -390,6 +405,22 @@ static int launch_simple(uint64_t seed, uint64_t sid, uint64_t offset, uint32_t 
     else k_gen_simple<1, Eval><<<grid, kGenBlock, 0, s>>>(a, out, ev);
     note_launch();
     return check_launch(what);
+}
+
+template <int D>
+static void launch_subdyadic(uint64_t seed, uint64_t sid, uint64_t offset, const float *coeffs, int K, int sub_bits,
+                             float *out, int64_t n, int mode, void *stream) {
+    const void *fn = mode == 8   ? (const void *)k_pcg32_subdyadic<D, 8>
+                     : mode == 4 ? (const void *)k_pcg32_subdyadic<D, 4>
+                                 : (const void *)k_pcg32_subdyadic<D, 1>;
+    const int grid = gen_grid(fn, n, mode);
+    const int64_t T = static_cast<int64_t>(grid) * kGenBlock;
+    const GenArgs a = make_gen_args(seed, sid, offset, n, T, mode == 1 ? 4 : mode);
+    uint32_t *o = reinterpret_cast<uint32_t *>(out);
+    cudaStream_t s = as_stream(stream);
+    if (mode == 8) k_pcg32_subdyadic<D, 8><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o);
+    else if (mode == 4) k_pcg32_subdyadic<D, 4><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o);
+    else k_pcg32_subdyadic<D, 1><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o);
 }
 
 }  // namespace arv
@@ -405,7 +436,7 @@ int arv_set_tuning(int key, int value) {
             g_group = value;
             return ARV_OK;
         case ARV_TUNE_CTAS_PER_SM:
-            if (value < 1 || value > 32) return set_error(ARV_ERR_CONFIG, "ctas_per_sm must be in [1, 32]");
+            if (value < 0 || value > 32) return set_error(ARV_ERR_CONFIG, "ctas_per_sm must be in [0 (auto), 32]");
             g_ctas_per_sm = value;
             return ARV_OK;
         default:
@@ -437,17 +468,17 @@ int arv_pcg32_constant_f32(uint64_t seed, uint64_t stream_id, uint64_t offset, c
     const int use_smem = q <= 14;
     const size_t smem = use_smem ? (sizeof(float) << q) : 0;
     const int mode = store_mode(out);
-    const int grid = gen_grid(n, mode);
+    const void *fn = mode == 8   ? (const void *)k_pcg32_constant<8>
+                     : mode == 4 ? (const void *)k_pcg32_constant<4>
+                                 : (const void *)k_pcg32_constant<1>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = gen_grid(fn, n, mode, smem);
     const int64_t T = static_cast<int64_t>(grid) * kGenBlock;
     const GenArgs a = make_gen_args(seed, stream_id, offset, n, T, mode == 1 ? 4 : mode);
     uint32_t *o = reinterpret_cast<uint32_t *>(out);
     cudaStream_t s = as_stream(stream);
 #define ARV_CONST(M)                                                                                        \
-    do {                                                                                                    \
-        if (smem > 48 * 1024)                                                                               \
-            cudaFuncSetAttribute(k_pcg32_constant<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        k_pcg32_constant<M><<<grid, kGenBlock, smem, s>>>(a, values, q, use_smem, o);                        \
-    } while (0)
+    k_pcg32_constant<M><<<grid, kGenBlock, smem, s>>>(a, values, q, use_smem, o)
     if (mode == 8) ARV_CONST(8);
     else if (mode == 4) ARV_CONST(4);
     else ARV_CONST(1);
@@ -464,25 +495,13 @@ int arv_pcg32_subdyadic_f32(uint64_t seed, uint64_t stream_id, uint64_t offset, 
     if (n < 0) return set_error(ARV_ERR_CONFIG, "negative n");
     if (n == 0) return ARV_OK;
     const int mode = store_mode(out);
-    const int grid = gen_grid(n, mode);
-    const int64_t T = static_cast<int64_t>(grid) * kGenBlock;
-    const GenArgs a = make_gen_args(seed, stream_id, offset, n, T, mode == 1 ? 4 : mode);
-    uint32_t *o = reinterpret_cast<uint32_t *>(out);
-    cudaStream_t s = as_stream(stream);
-#define ARV_SUB_CASE(D)                                                                               \
-    case D:                                                                                           \
-        if (mode == 8) k_pcg32_subdyadic<D, 8><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o);      \
-        else if (mode == 4) k_pcg32_subdyadic<D, 4><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o); \
-        else k_pcg32_subdyadic<D, 1><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o);                \
-        break;
     switch (degree) {
-        ARV_SUB_CASE(1)
-        ARV_SUB_CASE(2)
-        ARV_SUB_CASE(3)
-        ARV_SUB_CASE(4)
-        ARV_SUB_CASE(5)
+        case 1: launch_subdyadic<1>(seed, stream_id, offset, coeffs, K, sub_bits, out, n, mode, stream); break;
+        case 2: launch_subdyadic<2>(seed, stream_id, offset, coeffs, K, sub_bits, out, n, mode, stream); break;
+        case 3: launch_subdyadic<3>(seed, stream_id, offset, coeffs, K, sub_bits, out, n, mode, stream); break;
+        case 4: launch_subdyadic<4>(seed, stream_id, offset, coeffs, K, sub_bits, out, n, mode, stream); break;
+        default: launch_subdyadic<5>(seed, stream_id, offset, coeffs, K, sub_bits, out, n, mode, stream); break;
     }
-#undef ARV_SUB_CASE
     note_launch();
     return check_launch("arv_pcg32_subdyadic_f32");
 }
@@ -491,7 +510,7 @@ int arv_pcg32_gaussian_f64(uint64_t seed, uint64_t stream_id, uint64_t offset, d
     if (n < 0) return set_error(ARV_ERR_CONFIG, "negative n");
     if (n == 0) return ARV_OK;
     if (!aligned(out, 16)) return set_error(ARV_ERR_CONFIG, "arv_pcg32_gaussian_f64: out must be 16-byte aligned");
-    const int grid = stream_grid((n + 3) / 4, kGenBlock, g_ctas_per_sm);
+    const int grid = gen_grid((const void *)k_pcg32_gauss64, n, 4);
     const int64_t T = static_cast<int64_t>(grid) * kGenBlock;
     const GenArgs a = make_gen_args(seed, stream_id, offset, n, T, 4);
     k_pcg32_gauss64<<<grid, kGenBlock, 0, as_stream(stream)>>>(a, out);
@@ -503,7 +522,7 @@ int arv_store_probe_ex(float *out, int64_t n, int mode, void *stream) {
     if (n < 0 || (n & 7) || !aligned(out, 32)) return set_error(ARV_ERR_CONFIG, "store probe needs n % 8 == 0 and 32B alignment");
     if (n == 0) return ARV_OK;
     const int G = mode == 8 ? 8 : 4;
-    const int grid = stream_grid(n / G, kGenBlock, g_ctas_per_sm);
+    const int grid = gen_grid((const void *)k_store_probe<8>, n, G);
     uint32_t *o = reinterpret_cast<uint32_t *>(out);
     cudaStream_t s = as_stream(stream);
     if (mode == 8) k_store_probe<8><<<grid, kGenBlock, 0, s>>>(o, n);
