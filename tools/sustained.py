@@ -2,7 +2,7 @@
 launches for --seconds, timed in windows of --window launches with CUDA
 events, with NVML SM clock / power / throttle reasons sampled per window.
 
-    python tools/sustained.py [--n 268435456] [--seconds 5] [--window 50] [--kernel sub|const|store]
+    python tools/sustained.py [--n 268435456] [--seconds 5] [--window 50] [--kernel sub|const|words|store]
 """
 
 from __future__ import annotations
@@ -36,6 +36,8 @@ def main():
     s = torch.cuda.current_stream().cuda_stream
     if args.kernel == "store":
         fn = lambda: _native.call("arv_store_probe", out.data_ptr(), n, s)  # noqa: E731
+    elif args.kernel == "words":
+        fn = lambda: arv.Pcg32Stream(42, 0).words(n, out=out.view(torch.uint32))  # noqa: E731
     else:
         t = arv.load_table("subdyadic_linear_k16_s8" if args.kernel == "sub" else "constant_q10_l1")
         fn = lambda: arv.Pcg32Stream(42, 0).sample(t, n, out=out)  # noqa: E731
