@@ -32,7 +32,9 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 BYTES_PER_SAMPLE = 4  # algorithmic: one f32 store, PRNG state in registers
-METRIC = "approx-Gaussian ICDF samples/s (fused PCG32, f32 out)"
+# BASELINE.json "metric" verbatim; `value` is the whole-job aggregate (= per GPU at N=1),
+# the HBM-roofline fraction is in `roofline`, MLMC paths/s in `mlmc`.
+METRIC = "approx-Gaussian ICDF samples/s per GPU & % HBM roofline; MLMC paths/s"
 WORKLOADS = {
     # BASELINE.json configs[1] -- the headline (default)
     "config2": (1 << 28, "subdyadic_linear_k16_s8",
@@ -215,7 +217,7 @@ def run_reference(args) -> None:
     if int(os.environ.get("RANK", "0")) != 0:
         return
     threads = cpu_threads()
-    per_step = min(1 << 26, N_PER_GPU)
+    per_step = min(args.ref_samples, N_PER_GPU)
     for _ in range(max(args.warmup, 0)):
         cpu_port_rate(per_step, threads)
     t0 = time.perf_counter()
@@ -516,6 +518,8 @@ def main() -> None:
     ap.add_argument("--no-mlmc", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config2")
+    ap.add_argument("--ref-samples", type=int, default=1 << 26,
+                    help="reference arm: bounded host sample per step (samples)")
     args = ap.parse_args()
     select_workload(args.workload)
     if args.impl == "reference":
