@@ -395,6 +395,18 @@ def run_ours(args) -> None:
     s1.synchronize()
     store_gbs = n * 4 * 20 / (s0.elapsed_time(s1) * 1e-3) / 1e9
 
+    # sustained: the same launches back to back for ~2 s; the second half is
+    # past the board's power ramp (the generator reaches the power cap)
+    sustained = None
+    if not args.no_sustained:
+        sus_s, sus_clocks = sustained_per_launch(step, device, seconds=2.0)
+        st = torch.tensor([sus_s], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(st, op=dist.ReduceOp.MAX)
+        sustained = {"value": world * n / float(st.item()), "unit": "samples/s",
+                     "us_per_launch": float(st.item()) * 1e6, "window": "launches in t = 1..2 s of a 2 s run",
+                     "clocks": sus_clocks}
+
     mlmc = None if args.no_mlmc else mlmc_metrics(arv, args, rank, world, device)
 
     if world > 1:
@@ -427,6 +439,7 @@ def run_ours(args) -> None:
         "gpu_launches": int(launches),
         "clocks": sampler.summary(),
         "quality": quality,
+        "sustained": sustained,
     }
     if mlmc is not None:
         line["mlmc"] = mlmc
@@ -435,6 +448,28 @@ def run_ours(args) -> None:
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def sustained_per_launch(step, device, seconds: float = 2.0, window: int = 25):
+    """Mean per-launch time over the second half of `seconds` of back-to-back
+    launches (CUDA events per window of `window` launches), with NVML clocks."""
+    import torch
+
+    sampler = ClockSampler(device.index)
+    done, tail = 0.0, []
+    with sampler:
+        while done < seconds:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(window):
+                step()
+            b.record()
+            b.synchronize()
+            dt = a.elapsed_time(b) * 1e-3
+            done += dt
+            if done > seconds / 2:
+                tail.append(dt / window)
+    return statistics.mean(tail), sampler.summary()
 
 
 def approximation_error(arv, out, offset: int, chunk: int = 1 << 26) -> dict:
@@ -517,6 +552,7 @@ def main() -> None:
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-mlmc", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sustained", action="store_true")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config2")
     ap.add_argument("--ref-samples", type=int, default=1 << 26,
                     help="reference arm: bounded host sample per step (samples)")
