@@ -395,7 +395,10 @@ def run_ours(args) -> None:
     s1.synchronize()
     store_gbs = n * 4 * 20 / (s0.elapsed_time(s1) * 1e-3) / 1e9
 
-    # sustained: the same launches back to back for ~2 s; the second half is
+    mlmc = None if args.no_mlmc else mlmc_metrics(arv, args, rank, world, device)
+
+    # sustained (last GPU phase, so the power ramp cannot slow the MLMC timings):
+    # the same launches back to back for ~2 s; the second half is
     # past the board's power ramp (the generator reaches the power cap)
     sustained = None
     if not args.no_sustained:
@@ -407,7 +410,6 @@ def run_ours(args) -> None:
                      "us_per_launch": float(st.item()) * 1e6, "window": "launches in t = 1..2 s of a 2 s run",
                      "clocks": sus_clocks}
 
-    mlmc = None if args.no_mlmc else mlmc_metrics(arv, args, rank, world, device)
 
     if world > 1:
         dist.barrier()

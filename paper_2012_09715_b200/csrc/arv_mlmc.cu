@@ -277,10 +277,9 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(L
                                                                  double *__restrict__ paths,
                                                                  unsigned long long *__restrict__ n_fail) {
     extern __shared__ double smd[];
-    const NcTables nct = nc_tables_init(smd, A.nu_exact);  // kNcSmemDoubles doubles
     const double *tab = stacks;
     if (use_smem) {
-        double *st = smd + kNcSmemDoubles;
+        double *st = smd;
         const int64_t total = 2 * n_knots * (DEG + 1) * K1;
         for (int64_t k = threadIdx.x; k < total; k += blockDim.x) st[k] = __ldg(stacks + k);
         __syncthreads();
@@ -302,7 +301,7 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(L
             // mlmc.py:269-278 exact side, warm-started from the table
             const double lam_e = __dmul_rn(x_e, A.decay_over_scale);
             const double warm = ncchi2_eval1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_e);
-            const NcQuantile q = ncchi2_quantile(nct, u, A.nu_exact, lam_e, warm);
+            const NcQuantile q = ncchi2_quantile(u, A.nu_exact, lam_e, warm);
             fails += q.resid > 1e-8;
             x_e = __dmul_rn(A.scale, q.x);
         }
@@ -329,25 +328,21 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(L
 __global__ void __launch_bounds__(256) k_ncchi2_inv(const double *__restrict__ u, const double *__restrict__ lam,
                                                     int64_t nlam, double nu, const double *__restrict__ x0,
                                                     double *__restrict__ out, double *__restrict__ resid, int64_t n) {
-    extern __shared__ double smd[];
-    const NcTables nct = nc_tables_init(smd, nu);
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const double li = nlam == 1 ? lam[0] : lam[i];
-        const NcQuantile q = ncchi2_quantile(nct, u[i], nu, li, x0 ? x0[i] : -1.0);
+        const NcQuantile q = ncchi2_quantile(u[i], nu, li, x0 ? x0[i] : -1.0);
         out[i] = q.x;
         if (resid) resid[i] = q.resid;
     }
 }
 __global__ void __launch_bounds__(256) k_ncchi2_cdf(const double *__restrict__ x, const double *__restrict__ lam,
                                                     int64_t nlam, double nu, double *__restrict__ out, int64_t n) {
-    extern __shared__ double smd[];
-    const NcTables nct = nc_tables_init(smd, nu);
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const double li = nlam == 1 ? lam[0] : lam[i];
         const double xi = x[i];
-        out[i] = xi <= 0.0 ? 0.0 : ncchi2_cdf_minus(nct, xi, li, 0.0).resid;
+        out[i] = xi <= 0.0 ? 0.0 : ncchi2_cdf_minus(0.5 * nu, xi, nc_lam(li), 0.0).resid;
     }
 }
 
@@ -482,7 +477,7 @@ int arv_mlmc_cir_exact_level(const arv_level_spec *spec, const double *stacks, i
     double *parts = static_cast<double *>(workspace);
     const size_t bytes = sizeof(double) * 2 * n_knots * (degree + 1) * K1;
     const int use_smem = bytes <= 128 * 1024;
-    const size_t smem = sizeof(double) * kNcSmemDoubles + (use_smem ? bytes : 0);
+    const size_t smem = use_smem ? bytes : 0;
     cudaStream_t s = as_stream(stream);
     unsigned long long *nf = reinterpret_cast<unsigned long long *>(n_fail);
 #define ARV_CASE(D)                                                                                          \
@@ -510,8 +505,7 @@ int arv_ncchi2_inv_cdf(const double *u, const double *lam, int64_t nlam, double 
     if (!(nu > 0)) return set_error(ARV_ERR_DOMAIN, "degrees of freedom must be > 0");
     if (nlam != 1 && nlam != n) return set_error(ARV_ERR_CONFIG, "per-element lambda must match the shape of u");
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
-    const size_t smem = sizeof(double) * kNcSmemDoubles;
-    k_ncchi2_inv<<<stream_grid(n, 256, 8), 256, smem, as_stream(stream)>>>(u, lam, nlam, nu, x0, out, resid, n);
+    k_ncchi2_inv<<<stream_grid(n, 256, 8), 256, 0, as_stream(stream)>>>(u, lam, nlam, nu, x0, out, resid, n);
     note_launch();
     return check_launch("arv_ncchi2_inv_cdf");
 }
@@ -520,10 +514,21 @@ int arv_ncchi2_cdf(const double *x, const double *lam, int64_t nlam, double nu, 
     if (!(nu > 0)) return set_error(ARV_ERR_DOMAIN, "degrees of freedom must be > 0");
     if (nlam != 1 && nlam != n) return set_error(ARV_ERR_CONFIG, "per-element lambda must match the shape of x");
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
-    const size_t smem = sizeof(double) * kNcSmemDoubles;
-    k_ncchi2_cdf<<<stream_grid(n, 256, 8), 256, smem, as_stream(stream)>>>(x, lam, nlam, nu, out, n);
+    k_ncchi2_cdf<<<stream_grid(n, 256, 8), 256, 0, as_stream(stream)>>>(x, lam, nlam, nu, out, n);
     note_launch();
     return check_launch("arv_ncchi2_cdf");
 }
+
+#if ARV_NC_COUNT
+// diagnostic build only: {CDF evaluations, quantile solves} since the last call
+ARV_API int arv_nc_counters(unsigned long long *out) {
+    cudaMemcpyFromSymbol(out, g_nc_evals, sizeof(unsigned long long));
+    cudaMemcpyFromSymbol(out + 1, g_nc_solves, sizeof(unsigned long long));
+    const unsigned long long zero = 0;
+    cudaMemcpyToSymbol(g_nc_evals, &zero, sizeof zero);
+    cudaMemcpyToSymbol(g_nc_solves, &zero, sizeof zero);
+    return check_launch("arv_nc_counters");
+}
+#endif
 
 }  // extern "C"

@@ -15,52 +15,79 @@
 // Evaluation is ONE downward sweep over the index j with no incomplete-gamma
 // series or continued fraction: P(a, y) = sum_{n >= 0} G(a + n, y), so
 // starting at an index J where G(a0 + J, y) is negligible (above both the
-// Poisson window and y + 9 sqrt(y)) and adding
+// Poisson window and y + 8 sqrt(y)) and adding
 //     G(a0 + j - 1) = G(a0 + j) (a0 + j) / y
 // on the way down yields every P(a0 + j, y) as a sum of positive terms.  The
-// Poisson weights join at the window top k + 9 sqrt(h) + 10 (neglected mass
-// < 1e-17) through p_{j-1} = p_j j / h and are renormalised by their sum.
-// Per term ~9 FP64 operations, no division, no table load, no transcendental,
-// and every lane runs the same loop body (the earlier mode-centred version
-// with series / continued fraction for the mode term diverged 3:1 across
-// lanes: 172 ms -> 64 ms for the CIR level-6 kernel).  The only per-CDF
-// transcendentals are two exp and two log, with lgamma(j + 1) and
-// lgamma(a0 + j + 1) from per-CTA shared tables (j < kNcTab).
+// Poisson weights join at the window top k + 8 sqrt(h) + 10 (neglected mass
+// < ~1e-15) through p_{j-1} = p_j j / h and are renormalised by their sum.
+// Per window term 9 FP64 operations (the factor (a0 + j)/y is one FMA of the
+// exact index), no division, no table load, no transcendental, and every
+// lane runs the same loop body.  Everything that depends on lambda alone
+// (window, Poisson weight at its top) is set up once per quantile solve.
 //
-// Accuracy: P carries the relative rounding of exp/lgamma at J (~1e-12 at
-// lambda ~ 250), an absolute error well inside the 1e-8 residual contract;
-// Newton converges on this F itself, so tol_f is met on the device CDF.
+// The two starting values G(a0 + J, y) and Pois(top; h) are densities of the
+// form lam^x e^-lam / Gamma(x + 1) evaluated far from the mode.  Computed as
+// exp(x log lam - lam - lgamma(x + 1)) their relative error is the exponent's
+// magnitude times epsilon (5e-12 at lam ~ 1e4), so they use the saddle-point
+// form of C. Loader ("Fast and accurate computation of binomial
+// probabilities", 2000): exp(-stirlerr(x) - bd0(x, lam)) / sqrt(2 pi x) with
+// the Stirling remainder stirlerr and the deviance bd0 = x log(x/lam) + lam - x
+// summed by its series near x = lam -- relative error a few epsilon at any
+// magnitude, and no per-CTA lgamma tables.
 #pragma once
 
 #include "arv_common.cuh"
 
 namespace arv {
 
-constexpr int kNcTab = 1024;
+// stirlerr(n) = log Gamma(n + 1) - (n + 1/2) log n + n - log sqrt(2 pi):
+// exact values at n = 0..15 (50-digit evaluation), the asymptotic series
+// 1/(12n) - 1/(360n^3) + ... (5 terms, |error| < 2e-14 for n > 10) above,
+// lgamma for the remaining non-integer n <= 10 (not reached by the sweep:
+// its arguments are a0 + J > 10 and the integer window top).
+static __constant__ double kStirlerrInt[16] = {
+    0.0, 8.1061466795327258e-2, 4.1340695955409294e-2, 2.7677925684998339e-2,
+    2.0790672103765093e-2, 1.6644691189821192e-2, 1.3876128823070748e-2, 1.1896709945891770e-2,
+    1.0411265261972096e-2, 9.2554621827127329e-3, 8.3305634333628713e-3, 7.5736754879518408e-3,
+    6.9428401072095299e-3, 6.4089941880042071e-3, 5.9513701127588477e-3, 5.5547335519628014e-3};
 
-struct NcTables {
-    const double *lg_j;   // lgamma(j + 1)
-    const double *lg_aj;  // lgamma(a0 + j + 1)
-    double a0;
+__device__ inline double nc_stirlerr(double n) {
+    if (n <= 15.0 && n == floor(n)) return kStirlerrInt[static_cast<int>(n)];
+    if (n > 10.0) {
+        const double r = 1.0 / n, r2 = r * r;
+        return r * (1.0 / 12.0 - r2 * (1.0 / 360.0 - r2 * (1.0 / 1260.0 - r2 * (1.0 / 1680.0 - r2 * (1.0 / 1188.0)))));
+    }
+    constexpr double kLnSqrt2Pi = 0.918938533204672741780329736406;
+    return lgamma(n + 1.0) - (n + 0.5) * log(n) + n - kLnSqrt2Pi;
+}
 
-    __device__ __forceinline__ double lgj(int j) const {
-        return j < kNcTab ? lg_j[j] : lgamma(static_cast<double>(j) + 1.0);
+// bd0(x, m) = x log(x / m) + m - x; near x = m by its series in
+// v = (x - m)/(x + m): (x - m) v + 2 x v (v^2/3 + v^4/5 + ...), |v| < 0.1,
+// 8 terms (v^16/17 < 1e-17 of the leading term)
+__device__ inline double nc_bd0(double x, double m) {
+    const double d = x - m;
+    if (fabs(d) < 0.1 * (x + m)) {
+        const double v = d / (x + m);
+        const double v2 = v * v;
+        double t = 1.0 / 17.0;
+        t = fma(t, v2, 1.0 / 15.0);
+        t = fma(t, v2, 1.0 / 13.0);
+        t = fma(t, v2, 1.0 / 11.0);
+        t = fma(t, v2, 1.0 / 9.0);
+        t = fma(t, v2, 1.0 / 7.0);
+        t = fma(t, v2, 1.0 / 5.0);
+        t = fma(t, v2, 1.0 / 3.0);
+        return fma(2.0 * x * v, v2 * t, d * v);
     }
-    __device__ __forceinline__ double lgaj(int j) const {
-        return j < kNcTab ? lg_aj[j] : lgamma(a0 + static_cast<double>(j) + 1.0);
-    }
-};
+    return x * log(x / m) + m - x;
+}
 
-// Fill the tables in shared memory (kNcSmemDoubles doubles) for a0 = nu / 2.
-constexpr int kNcSmemDoubles = 2 * kNcTab;
-__device__ inline NcTables nc_tables_init(double *sm, double nu) {
-    const double a0 = 0.5 * nu;
-    for (int j = threadIdx.x; j < kNcTab; j += blockDim.x) {
-        sm[j] = lgamma(static_cast<double>(j) + 1.0);
-        sm[kNcTab + j] = lgamma(a0 + static_cast<double>(j) + 1.0);
-    }
-    __syncthreads();
-    return {sm, sm + kNcTab, a0};
+// log(m^x e^-m / Gamma(x + 1)) for real x >= 0, m >= 0
+__device__ inline double nc_logdens(double x, double m) {
+    if (m <= 0.0) return x == 0.0 ? 0.0 : -INFINITY;
+    if (x == 0.0) return -m;
+    constexpr double kTwoPi = 6.283185307179586476925286766559;
+    return -nc_stirlerr(x) - nc_bd0(x, m) - 0.5 * log(kTwoPi * x);
 }
 
 struct NcCdf {
@@ -68,42 +95,86 @@ struct NcCdf {
     double pdf;
 };
 
-// F(x) - u and f(x) for x > 0.
-__device__ inline NcCdf ncchi2_cdf_minus(const NcTables &t, double x, double lam, double u) {
+// Half-width of the Poisson window and height of the gamma sweep above y, in
+// standard deviations (+10 terms): 8 sigma leaves < ~1e-15 of either mass.
+#ifndef ARV_NC_SIGMAS
+#define ARV_NC_SIGMAS 8.0
+#endif
+constexpr double kNcSigmas = ARV_NC_SIGMAS;
+
+// The lambda-only part of the CDF: Poisson window [bot, top] around
+// k = floor(lambda/2) and the weight at its top.  Fixed during a quantile
+// solve, so it is computed once per (u, lambda), not once per Newton step.
+struct NcLam {
+    double h, inv_h, p_top;
+    int top, bot;
+};
+
+__device__ inline NcLam nc_lam(double lam) {
+    NcLam L;
+    L.h = 0.5 * lam;
+    const int k = static_cast<int>(floor(L.h));
+    const int wp = L.h < 1e-2 ? 8 : static_cast<int>(kNcSigmas * sqrt(L.h)) + 10;
+    L.top = k + wp;
+    L.bot = k - wp > 0 ? k - wp : 0;
+    L.inv_h = L.h > 0.0 ? 1.0 / L.h : 0.0;
+    L.p_top = L.h > 0.0 ? exp(nc_logdens(static_cast<double>(L.top), L.h)) : 0.0;
+    return L;
+}
+
+// F(x) - u and f(x) for x > 0, a0 = nu / 2.
+__device__ inline NcCdf ncchi2_cdf_minus(double a0, double x, const NcLam &L, double u) {
     const double y = 0.5 * x;
-    const double a0 = t.a0;
-    const double h = 0.5 * lam;
-    const double kd = floor(h);
-    const int k = static_cast<int>(kd);
-    const int wp = h < 1e-2 ? 8 : static_cast<int>(9.0 * sqrt(h)) + 10;
-    const int top = k + wp;
-    const int bot = k - wp > 0 ? k - wp : 0;
-    const int jy = static_cast<int>(ceil(y - a0)) + static_cast<int>(9.0 * sqrt(y)) + 10;
-    const int J = jy > top ? jy : top;
+    const int top = L.top, bot = L.bot;
+    const int jy = static_cast<int>(ceil(y - a0)) + static_cast<int>(kNcSigmas * sqrt(y)) + 10;
+    int j = jy > top ? jy : top;
     const double inv_y = 1.0 / y;
-    const double inv_h = h > 0.0 ? 1.0 / h : 0.0;
-    double G = exp((a0 + static_cast<double>(J)) * log(y) - y - t.lgaj(J));  // G(a0 + J)
-    double P = G;                                                           // P(a0 + J) ~ G(a0 + J)
-    double jd = static_cast<double>(J);
-    for (int j = J; j > top; --j) {  // above the Poisson window: P and G only
-        G *= (a0 + jd) * inv_y;
+    const double a0y = a0 * inv_y;
+    double jd = static_cast<double>(j);
+    // G(a0 + J).  Far left tail (y << a0 + J) it underflows and the recurrence
+    // would stay at zero: walk down in log space to the first representable
+    // term; everything above it is below e^-700 of the retained terms.
+    double lg = nc_logdens(a0 + jd, y);
+    while (lg < -700.0 && j > 0) {
+        lg += log(fma(jd, inv_y, a0y));
+        jd -= 1.0;
+        --j;
+    }
+    double G = exp(lg);
+    double P = G;                    // P(a0 + j) ~ G(a0 + j)
+    for (; j > top; --j) {           // above the Poisson window: P and G only
+        G *= fma(jd, inv_y, a0y);    // G(a0 + j - 1) = G(a0 + j) (a0 + j) / y
         P += G;
         jd -= 1.0;
     }
-    // Poisson weight at the window top (h > 0); h == 0 is the central law (p_0 = 1)
-    double p = h > 0.0 ? exp(-h + jd * log(h) - t.lgj(top)) : (top == 0 ? 1.0 : 0.0);
-    double wsum = 0.0, acc = 0.0, dens = 0.0;
-    for (int j = top; j >= bot; --j) {
-        wsum += p;
-        acc += p * P;
-        const double Gm = G * (a0 + jd) * inv_y;  // G(a0 + j - 1)
-        dens += p * Gm;
-        P += Gm;
-        G = Gm;
-        p = h > 0.0 ? p * jd * inv_h : (j == 1 ? 1.0 : 0.0);
+    if (L.h > 0.0) {
+        const double inv_h = L.inv_h;
+        double p = L.p_top;
+        double wsum = 0.0, acc = 0.0, dens = 0.0;
+        for (int i = top; i > j && i >= bot; --i) {  // window indices whose gamma terms underflowed
+            wsum += p;
+            p *= static_cast<double>(i) * inv_h;
+        }
+        for (; j >= bot; --j) {
+            wsum += p;
+            acc = fma(p, P, acc);
+            const double Gm = G * fma(jd, inv_y, a0y);  // G(a0 + j - 1)
+            dens = fma(p, Gm, dens);
+            P += Gm;
+            G = Gm;
+            p *= jd * inv_h;
+            jd -= 1.0;
+        }
+        const double inv_w = 1.0 / wsum;
+        return {fma(acc, inv_w, -u), 0.5 * dens * inv_w};
+    }
+    // h == 0: the central law, F = P(a0, y), f = G(a0 - 1, y) / 2
+    for (; j > 0; --j) {
+        G *= fma(jd, inv_y, a0y);
+        P += G;
         jd -= 1.0;
     }
-    return {acc / wsum - u, 0.5 * dens / wsum};
+    return {P - u, 0.5 * G * a0y};
 }
 
 struct NcQuantile {
@@ -111,15 +182,21 @@ struct NcQuantile {
     double resid;  // |F(x) - u|
 };
 
+#if ARV_NC_COUNT  // diagnostic build: CDF evaluations and window terms
+__device__ unsigned long long g_nc_evals, g_nc_solves;
+#endif
+
 // exact_dist.py:381-461 contract, per element, warm start x0 (<= 0: mean).
-__device__ inline NcQuantile ncchi2_quantile(const NcTables &t, double u, double nu, double lam, double x0) {
+__device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, double x0) {
+    const double a0 = 0.5 * nu;
     const double one_minus_u = 1.0 - u;
     double hi = lam + nu + 20.0 * sqrt(2.0 * (lam + nu)) + 100.0;
     double lo = 0.0;
     const double tol_f = fmin(1e-9, fmax(1e-13, 1e-4 * fmin(u, one_minus_u)));
     double x = x0 > 0.0 ? x0 : lam + nu;
     x = fmin(fmax(x, 1e-8), hi);
-    NcCdf c = ncchi2_cdf_minus(t, x, lam, u);
+    const NcLam L = nc_lam(lam);
+    NcCdf c = ncchi2_cdf_minus(a0, x, L, u);
     for (int it = 0; it < 80; ++it) {
         if (fabs(c.resid) <= tol_f) break;
         if (c.resid > 0.0) hi = x;
@@ -127,9 +204,16 @@ __device__ inline NcQuantile ncchi2_quantile(const NcTables &t, double u, double
         double xn = x - c.resid / c.pdf;
         if (!isfinite(xn) || xn <= lo || xn >= hi) xn = 0.5 * (lo + hi);
         x = xn;
-        c = ncchi2_cdf_minus(t, x, lam, u);
+        c = ncchi2_cdf_minus(a0, x, L, u);
+#if ARV_NC_COUNT
+        atomicAdd(&g_nc_evals, 1ull);
+#endif
         if (hi - lo < 1e-15 * hi) break;
     }
+#if ARV_NC_COUNT
+    atomicAdd(&g_nc_evals, 1ull);
+    atomicAdd(&g_nc_solves, 1ull);
+#endif
     return {x, fabs(c.resid)};
 }
 

@@ -83,14 +83,14 @@ def test_cir_exact_paths_match_reference(arv, golden, hashes):
         np.testing.assert_allclose(b.p_fine_exact.cpu().numpy(), ref[0], rtol=1e-7)
 
 
-def test_device_ncchi2_quantile_contract(arv):
+@pytest.mark.parametrize("nu", [4 * 0.5 * 0.04 / 0.2**2, 0.7, 5.0])
+def test_device_ncchi2_quantile_contract(arv, nu):
     """|chndtr(x) - u| <= 1e-8 (exact_dist.py:454-460) on a (u, lam) grid incl. tails."""
     from scipy import special as sp
 
     from paper_2012_09715_b200 import _device as dev
     from paper_2012_09715_b200._native import call
 
-    nu = 4 * 0.5 * 0.04 / 0.2**2
     u = np.concatenate([np.linspace(1e-6, 1 - 1e-6, 301), [1e-10, 1e-9, 1e-8, 1 - 1e-8, 1 - 1e-9, 0.5]])
     # 5000 and 20000 push the Poisson window past the per-CTA reciprocal/lgamma tables
     for lam in (0.0, 1e-6, 0.5, 3.0, 30.0, 250.0, 1000.0, 5000.0, 20000.0):
@@ -104,6 +104,32 @@ def test_device_ncchi2_quantile_contract(arv):
         resid = np.abs(sp.chndtr(x, nu, lam) - u)
         assert resid.max() <= 1e-8, (lam, resid.max(), u[np.argmax(resid)])
         assert rd.cpu().numpy().max() <= 1e-8
+
+
+@pytest.mark.parametrize("nu", [4 * 0.5 * 0.04 / 0.2**2, 1.0, 7.3])
+def test_device_ncchi2_cdf_accuracy(arv, nu):
+    """The device Poisson-gamma sweep against scipy's CDFLIB chndtr across
+    lambda from 0 to 2e4 and x from the far left to the far right tail.  The
+    reference's own series-vs-CDFLIB tolerance is 5e-12 (test_exact_dist.py:
+    154-160); the saddle-point start values keep the sweep within 1e-12."""
+    from scipy import special as sp
+
+    from paper_2012_09715_b200 import _device as dev
+    from paper_2012_09715_b200._native import call
+
+    worst = 0.0
+    for lam in (0.0, 1e-6, 0.5, 3.0, 30.0, 250.0, 1000.0, 5000.0, 20000.0):
+        mean, sd = lam + nu, math.sqrt(2 * (nu + 2 * lam))
+        x = np.concatenate([np.linspace(max(mean - 8 * sd, 1e-6), mean + 10 * sd, 997), [1e-8, 1e-3, 0.1]])
+        x = x[x > 0]
+        xd = torch.from_numpy(x).cuda()
+        ld = torch.full((1,), lam, dtype=torch.float64, device="cuda")
+        od = torch.empty_like(xd)
+        call("arv_ncchi2_cdf", xd.data_ptr(), ld.data_ptr(), 1, nu, od.data_ptr(), xd.numel(), dev.stream_handle())
+        err = np.abs(od.cpu().numpy() - sp.chndtr(x, nu, lam))
+        worst = max(worst, float(err.max()))
+        print(f"nu={nu:.4g} lam={lam:g}: max |F_dev - chndtr| = {err.max():.3g}")
+        assert err.max() <= 1e-12, (lam, err.max(), x[np.argmax(err)])
 
 
 def test_level_stats_match_per_path(arv):

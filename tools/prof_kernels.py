@@ -100,6 +100,12 @@ def main():
         sp = arv.LevelSpec(level=6, scheme="cir_exact", process=arv.CirParams(0.5, 0.04, 0.2, 0.04, 1.0),
                            rv_source=tab, kind="four_way", n0=1)
         res["cir_l6"] = timed(lambda: run_level(sp, arv.level_stream(42, 6), 1 << 20), args.reps)
+    if "cirall" in which:  # config 5: every level, 2^20 paths
+        tab = arv.load_table("ncchi2_cir_k64_stacks")
+        for lv in range(7):
+            sp = arv.LevelSpec(level=lv, scheme="cir_exact", process=arv.CirParams(0.5, 0.04, 0.2, 0.04, 1.0),
+                               rv_source=tab, kind="four_way", n0=1)
+            res[f"cir_l{lv}"] = timed(lambda: run_level(sp, arv.level_stream(42, lv), 1 << 20), args.reps)
     for k, v in res.items():
         print(f"{k}: {v:.4f} ms")
 
