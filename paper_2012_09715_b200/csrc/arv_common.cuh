@@ -207,6 +207,14 @@ __device__ __forceinline__ double u32_to_f64(uint32_t w) {
     return __dmul_rn(__dadd_rn(static_cast<double>(w), 0.5), 0x1p-32);
 }
 
+// The same f64 uniform as D = 1 + u assembled from the word's bits (sign 0,
+// exponent 0x3FF, mantissa w . 1 . 0...): exact, so D - 1 == u32_to_f64(w)
+// bit for bit without the I2F and DMUL; the reference's u > 1/2 is w >= 2^31
+// (both pinned by tests/test_oracle.py::test_f64_uniform_integer_domain).
+__device__ __forceinline__ double one_plus_u32(uint32_t w) {
+    return __hiloint2double(static_cast<int>(0x3FF00000u | (w >> 12)), static_cast<int>((w << 20) | 0x80000u));
+}
+
 // ------------------------------------------------------ AS 241 (PPND16) --
 // exact_dist.py:30-62 coefficients (constant term first); evaluation order of
 // exact_dist.py:65-126.  Coefficients live in constant memory: every lane of
@@ -287,10 +295,9 @@ __device__ __forceinline__ double as241_f64_branchy(double u) {
 // division keep the reference's operation order, so every lane is rounded
 // exactly as in as241_f64_branchy.  Only the log/sqrt of the tail and the
 // r > 5 far tail (u < ~1.4e-11) stay divergent.
-__device__ __forceinline__ double as241_f64(double u) {
-    const double q = __dsub_rn(u, 0.5);
-    const bool central = fabs(q) <= 0.425;
-    const bool upper = u > 0.5;
+// Core with the region predicates and q = u - 1/2 supplied by the caller
+// (the PCG32 level kernels derive u > 1/2 from the word).
+__device__ __forceinline__ double as241_f64_core(double u, double q, bool central, bool upper) {
     double x;
     if (central) {
         x = __dsub_rn(0.180625, __dmul_rn(q, q));
@@ -323,6 +330,11 @@ __device__ __forceinline__ double as241_f64(double u) {
 #endif
     const double val = __ddiv_rn(central ? __dmul_rn(q, num) : num, den);
     return central || upper ? val : -val;
+}
+
+__device__ __forceinline__ double as241_f64(double u) {
+    const double q = __dsub_rn(u, 0.5);
+    return as241_f64_core(u, q, fabs(q) <= 0.425, u > 0.5);
 }
 
 __device__ __forceinline__ float as241_f32_branchy(float u) {

@@ -6,9 +6,10 @@
 namespace arv {
 
 // _kernels.pyx:56-73 for one element; coefficient table `c` (DEG+1, K1).
+// `pred` is the reference's u < 0.5 (callers with the PCG32 word pass it from
+// an integer compare).
 template <int DEG>
-__device__ __forceinline__ double dyadic_eval1(const double *c, int64_t K1, double ui) {
-    const bool pred = ui < 0.5;
+__device__ __forceinline__ double dyadic_eval1(const double *c, int64_t K1, double ui, bool pred) {
     const double v = pred ? ui : __dsub_rn(1.0, ui);
     long long idx = dyadic_idx64(v, K1 - 1);
     idx = idx < 0 ? 0 : idx;
@@ -17,20 +18,28 @@ __device__ __forceinline__ double dyadic_eval1(const double *c, int64_t K1, doub
     for (int d = DEG - 1; d >= 0; --d) z = __dadd_rn(__dmul_rn(z, v), c[d * K1 + idx]);
     return pred ? z : -z;
 }
+template <int DEG>
+__device__ __forceinline__ double dyadic_eval1(const double *c, int64_t K1, double ui) {
+    return dyadic_eval1<DEG>(c, K1, ui, ui < 0.5);
+}
 
 // Approximate-side Gaussian table of the path kernels: DEG >= 1 is a dyadic
 // table (degree+1, K1) evaluated as dyadic_eval; DEG == 0 is a piecewise-
 // constant table values[K1] evaluated as constant_eval (_kernels.pyx:16-23).
 template <int DEG>
-__device__ __forceinline__ double gauss_table_eval(const double *c, int64_t K1, double u) {
+__device__ __forceinline__ double gauss_table_eval(const double *c, int64_t K1, double u, bool lower) {
     if constexpr (DEG == 0) {
         long long idx = static_cast<long long>(__dmul_rn(static_cast<double>(K1), u));
         idx = idx < K1 ? idx : K1 - 1;
         idx = idx < 0 ? 0 : idx;
         return c[idx];
     } else {
-        return dyadic_eval1<DEG>(c, K1, u);
+        return dyadic_eval1<DEG>(c, K1, u, lower);
     }
+}
+template <int DEG>
+__device__ __forceinline__ double gauss_table_eval(const double *c, int64_t K1, double u) {
+    return gauss_table_eval<DEG>(c, K1, u, u < 0.5);
 }
 
 // _kernels.pyx:96-143 for one element.  stacks (2, n_knots, DEG+1, K1):

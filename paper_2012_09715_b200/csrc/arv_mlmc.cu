@@ -78,6 +78,49 @@ struct PathRng {
     }
 };
 
+// Compile-time uniform source of the Gaussian-scheme kernels: the PCG32 side
+// keeps the raw word, so the f64 uniform is assembled from its bits and the
+// u < 1/2 predicates are integer compares (-2% on the GBM level kernel).
+template <bool PHILOX>
+struct PathSource;
+
+template <>
+struct PathSource<false> {
+    uint64_t s;
+    Affine step;
+    __device__ __forceinline__ PathSource(const LevelArgs &A, uint64_t p) : step(A.step) {
+        const Affine jp = lcg_jump(p, A.inc);
+        s = jp.a * A.s0 + jp.c;
+    }
+    // exact (AS241) and table normals of the next uniform
+    template <int DEG>
+    __device__ __forceinline__ void normals(const double *tab, int64_t K1, double &z, double &a) {
+        const uint32_t w = pcg32_output(s);
+        s = step.a * s + step.c;
+        const double u = __dsub_rn(one_plus_u32(w), 1.0);  // == u32_to_f64(w), no I2F / DMUL
+        const double q = __dsub_rn(u, 0.5);
+        // u > 1/2 <=> w >= 2^31 (integer compare instead of DSETP).  The
+        // central-region test stays in f64: as an integer compare it changes
+        // ptxas' schedule of the rare far-tail branch and spills (measured).
+        z = as241_f64_core(u, q, fabs(q) <= 0.425, w >= 0x80000000u);
+        a = gauss_table_eval<DEG>(tab, K1, u, w < 0x80000000u);
+    }
+};
+
+template <>
+struct PathSource<true> {
+    uint64_t s, n_paths, seed, sid;
+    __device__ __forceinline__ PathSource(const LevelArgs &A, uint64_t p)
+        : s(p), n_paths(A.n_paths_total), seed(A.seed), sid(A.sid) {}
+    template <int DEG>
+    __device__ __forceinline__ void normals(const double *tab, int64_t K1, double &z, double &a) {
+        const double u = u64_to_f64(philox_word(s, seed, sid));  // sampler.py:62
+        s += n_paths;
+        z = as241_f64(u);
+        a = gauss_table_eval<DEG>(tab, K1, u);
+    }
+};
+
 __device__ __forceinline__ double payoff_fn(double x, int payoff, double strike) {
     return payoff == ARV_PAYOFF_CALL ? fmax(__dsub_rn(x, strike), 0.0) : x;
 }
@@ -212,7 +255,7 @@ __global__ void __launch_bounds__(kFinalBlock) k_finalize(const double *__restri
 
 // --------------------------------------------------- Gaussian schemes --
 // SCHEME: ARV_SCHEME_EM, _MILSTEIN (GBM), _CIR_EULER_TRUNCATED, _CIR_MILSTEIN_TRUNCATED
-template <int DEG, int SCHEME>
+template <int DEG, int SCHEME, bool PHILOX>
 __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_MINB) k_gaussian_level(LevelArgs A, const double *__restrict__ coeffs,
                                                                 int64_t K1, double *__restrict__ parts,
                                                                 double *__restrict__ paths) {
@@ -227,7 +270,7 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_MINB) k_gaussian_level(Le
     double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (valid) {
         const uint64_t p = static_cast<uint64_t>(A.path_lo + i);
-        PathRng rng(A, p);
+        PathSource<PHILOX> rng(A, p);
         const double x0 = A.x0, dt_f = A.dt_f, dt_c = A.dt_c, sq_f = A.sq_f;
         double xf_e = x0, xc_e = x0, xf_a = x0, xc_a = x0;
         auto step = [&](double x, double dw, double dt) -> double {
@@ -235,19 +278,19 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_MINB) k_gaussian_level(Le
             else return cir_step<MIL>(x, dw, dt, A.a, A.b, A.c);
         };
         for (int64_t pair = 0; pair < A.n_f / 2; ++pair) {
-            const double u1 = rng.next();
-            const double u2 = rng.next();
-            const double z1 = as241_f64(u1), z2 = as241_f64(u2);
+            double z1, w1, z2, w2;  // exact / table normals of the same uniform
+            rng.template normals<DEG>(smd, K1, z1, w1);
+            rng.template normals<DEG>(smd, K1, z2, w2);
             xf_e = step(step(xf_e, __dmul_rn(sq_f, z1), dt_f), __dmul_rn(sq_f, z2), dt_f);
             xc_e = step(xc_e, __dmul_rn(sq_f, __dadd_rn(z1, z2)), dt_c);
-            const double w1 = gauss_table_eval<DEG>(smd, K1, u1), w2 = gauss_table_eval<DEG>(smd, K1, u2);
             xf_a = step(step(xf_a, __dmul_rn(sq_f, w1), dt_f), __dmul_rn(sq_f, w2), dt_f);
             xc_a = step(xc_a, __dmul_rn(sq_f, __dadd_rn(w1, w2)), dt_c);
         }
         if (A.n_f & 1) {
-            const double u1 = rng.next();
-            xf_e = step(xf_e, __dmul_rn(sq_f, as241_f64(u1)), dt_f);
-            xf_a = step(xf_a, __dmul_rn(sq_f, gauss_table_eval<DEG>(smd, K1, u1)), dt_f);
+            double z1, w1;
+            rng.template normals<DEG>(smd, K1, z1, w1);
+            xf_e = step(xf_e, __dmul_rn(sq_f, z1), dt_f);
+            xf_a = step(xf_a, __dmul_rn(sq_f, w1), dt_f);
         }
         const double fe = payoff_fn(xf_e, A.payoff, A.strike);
         const double fa = payoff_fn(xf_a, A.payoff, A.strike);
@@ -426,7 +469,10 @@ int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, in
     double *parts = static_cast<double *>(workspace);
     const size_t smem = sizeof(double) * (degree + 1) * K1;
     cudaStream_t s = as_stream(stream);
-#define ARV_LAUNCH(D, S) k_gaussian_level<D, S><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths)
+#define ARV_LAUNCH(D, S)                                                                              \
+    (A.rng == ARV_RNG_PHILOX                                                                          \
+         ? k_gaussian_level<D, S, true><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths) \
+         : k_gaussian_level<D, S, false><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths))
 #define ARV_SCHEMES(D)                                                                      \
     case D:                                                                                 \
         switch (scheme) {                                                                   \

@@ -40,6 +40,27 @@ class TestPcg32:
         m = (1 << 64) - 1
         assert a == (a2 * a1) & m and c == (a2 * c1 + c2) & m
 
+    def test_f64_uniform_integer_domain(self, orc):
+        """one_plus_u32 (arv_common.cuh): D = 1 + u assembled from the word's bits,
+        u - 1/2 = D - 3/2, and AS241's |u - 1/2| <= 0.425 / u > 1/2 as integer
+        compares on w -- all equal to the reference's f64 arithmetic."""
+        lo, span = 322122547, 3650722201
+        edges = [0, 1, 2**31 - 1, 2**31, 2**31 + 1, 2**32 - 1, lo - 1, lo, lo + 1, lo + span - 1, lo + span,
+                 lo + span + 1]
+        rng = np.random.default_rng(11)
+        w = np.concatenate([np.array(edges, dtype=np.uint64), rng.integers(0, 2**32, 200_000, dtype=np.uint64)])
+        w = w.astype(np.uint32)
+        u = orc.u32_to_f64(w)  # (w + 1/2) 2^-32, the reference-order f64 map
+        d_bits = (np.uint64(0x3FF00000) | (w.astype(np.uint64) >> np.uint64(12))) << np.uint64(32) | \
+            ((w.astype(np.uint64) << np.uint64(20)) & np.uint64(0xFFFFFFFF)) | np.uint64(0x80000)
+        D = d_bits.view(np.float64)
+        assert np.array_equal(bits(D - 1.0), bits(u))
+        assert np.array_equal(bits(D - 1.5), bits(u - 0.5))
+        assert np.array_equal(bits(2.0 - D), bits(1.0 - u))
+        central = ((w.astype(np.int64) - lo) % 2**32) <= span
+        assert np.array_equal(central, np.abs(u - 0.5) <= 0.425)
+        assert np.array_equal(w >= np.uint32(2**31), u > 0.5)
+
     def test_lattice_mapping(self, orc, golden):
         u = orc.u32_to_f32(golden["lattice_words"])
         assert np.array_equal(bits(u), bits(golden["lattice_u32"]))
