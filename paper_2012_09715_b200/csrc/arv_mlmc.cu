@@ -25,6 +25,9 @@ namespace arv {
 
 constexpr int kLevelBlock = 256;
 // Min resident CTAs per SM (register cap) for the level kernels; see sweeps.
+#ifndef ARV_GBM_MINB_PCG  // GBM + PCG32 instances fit 64 registers without spills (1.3% faster)
+#define ARV_GBM_MINB_PCG 4
+#endif
 #ifndef ARV_GBM_MINB
 #define ARV_GBM_MINB 3
 #endif
@@ -256,7 +259,9 @@ __global__ void __launch_bounds__(kFinalBlock) k_finalize(const double *__restri
 // --------------------------------------------------- Gaussian schemes --
 // SCHEME: ARV_SCHEME_EM, _MILSTEIN (GBM), _CIR_EULER_TRUNCATED, _CIR_MILSTEIN_TRUNCATED
 template <int DEG, int SCHEME, bool PHILOX>
-__global__ void __launch_bounds__(kLevelBlock, ARV_GBM_MINB) k_gaussian_level(LevelArgs A, const double *__restrict__ coeffs,
+__global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEME == ARV_SCHEME_MILSTEIN) && !PHILOX
+                                                   ? ARV_GBM_MINB_PCG
+                                                   : ARV_GBM_MINB) k_gaussian_level(LevelArgs A, const double *__restrict__ coeffs,
                                                                 int64_t K1, double *__restrict__ parts,
                                                                 double *__restrict__ paths) {
     extern __shared__ double smd[];
