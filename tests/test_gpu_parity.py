@@ -105,8 +105,21 @@ class TestFusedGenerators:
         err = out.double() - ex
         rmse = float(torch.sqrt(torch.mean(err * err)))
         assert 2e-4 < rmse < 6e-4
-        # antisymmetry on the lattice is structural: the top and bottom halves are mirror images
         assert bool(torch.isfinite(out).all())
+
+    def test_antisymmetry_on_the_lattice(self, arv, orc, tables_npz):
+        """test_sampler.py:137-139 / helpers.py:64-68: z(1 - u) == -z(u) bit for bit.
+        The mirror of lattice word w is ~w (u -> 1 - u exactly), so the fused
+        output of a stream is checked against the drop-in evaluator on 1 - u."""
+        n = 1 << 20
+        t = arv.load_table("subdyadic_linear_k16_s8")
+        out = arv.Pcg32Stream(3, 8).sample(t, n).cpu().numpy()
+        u = orc.u32_to_f32(orc.pcg32_words(3, 8, 0, n))
+        mirrored = (np.float32(1.0) - u).astype(np.float32)
+        assert np.array_equal(orc.u32_to_f32(~orc.pcg32_words(3, 8, 0, n)), mirrored)
+        got = np.empty_like(mirrored)
+        arv.get_kernels().subdyadic_eval32(tables_npz["subdyadic_linear_k16_s8"].astype(np.float32), 3, mirrored, got)
+        assert np.array_equal(bits(got), bits(-out))
 
     @pytest.mark.parametrize("n", [1, 2, 7, 8, 9, 15, 31, 33, 1023, 4097])
     @pytest.mark.parametrize("pad", [0, 1, 4])  # element offset into the buffer: v8 / scalar / v4 store paths
