@@ -244,12 +244,55 @@ static __constant__ double kAS241d[6][8] = {{ARV_AS241_A}, {ARV_AS241_B}, {ARV_A
 static __constant__ float kAS241f[6][8] = {{ARV_AS241_A}, {ARV_AS241_B}, {ARV_AS241_C},
                                            {ARV_AS241_D}, {ARV_AS241_E}, {ARV_AS241_F}};
 
-// A|B|C|D rows (central num/den, near-tail num/den) in global memory for the
-// per-lane coefficient loads of as241_f64.
-#ifndef ARV_AS241_SELECT
-#define ARV_AS241_SELECT 0
-#endif
-static __device__ const double kAS241g[32] = {ARV_AS241_A, ARV_AS241_B, ARV_AS241_C, ARV_AS241_D};
+// Per-lane coefficient rows for as241_f64 / as241_f32 in global memory,
+// interleaved (A_i, B_i) for the central rational and (C_i, D_i) for the near
+// tail, so one 16-byte (f64) or 8-byte (f32) read-only load feeds both Horner
+// chains at step i.  A warp touches at most the two rows: L1-resident.
+template <typename T>
+struct alignas(2 * sizeof(T)) AS241Pairs {
+    T v[32];
+};
+template <typename T>
+constexpr AS241Pairs<T> as241_pairs() {
+    constexpr double A[8] = {ARV_AS241_A}, B[8] = {ARV_AS241_B}, C[8] = {ARV_AS241_C}, D[8] = {ARV_AS241_D};
+    AS241Pairs<T> p{};
+    for (int i = 0; i < 8; ++i) {
+        p.v[2 * i] = static_cast<T>(A[i]);
+        p.v[2 * i + 1] = static_cast<T>(B[i]);
+        p.v[16 + 2 * i] = static_cast<T>(C[i]);
+        p.v[16 + 2 * i + 1] = static_cast<T>(D[i]);
+    }
+    return p;
+}
+static __device__ const AS241Pairs<double> kAS241pd = as241_pairs<double>();
+static __device__ const AS241Pairs<float> kAS241pf = as241_pairs<float>();
+
+// num(x) / den(x) of the lane's rational (central A/B or near-tail C/D),
+// Horner with separately rounded multiply and add in the reference's order.
+__device__ __forceinline__ void as241_rational(double x, bool central, double &num, double &den) {
+    const double2 *cf = reinterpret_cast<const double2 *>(kAS241pd.v) + (central ? 0 : 8);
+    double2 c = __ldg(cf + 7);
+    num = c.x;
+    den = c.y;
+#pragma unroll
+    for (int i = 6; i >= 0; --i) {
+        c = __ldg(cf + i);
+        num = __dadd_rn(__dmul_rn(num, x), c.x);
+        den = __dadd_rn(__dmul_rn(den, x), c.y);
+    }
+}
+__device__ __forceinline__ void as241_rational(float x, bool central, float &num, float &den) {
+    const float2 *cf = reinterpret_cast<const float2 *>(kAS241pf.v) + (central ? 0 : 8);
+    float2 c = __ldg(cf + 7);
+    num = c.x;
+    den = c.y;
+#pragma unroll
+    for (int i = 6; i >= 0; --i) {
+        c = __ldg(cf + i);
+        num = __fadd_rn(__fmul_rn(num, x), c.x);
+        den = __fadd_rn(__fmul_rn(den, x), c.y);
+    }
+}
 
 // Horner with separately rounded multiply and add (numpy has no FMA).
 __device__ __forceinline__ double poly8d(int which, double x) {
@@ -307,27 +350,8 @@ __device__ __forceinline__ double as241_f64_core(double u, double q, bool centra
         if (r > 5.0) return as241_f64_branchy(u);
         x = __dsub_rn(r, 1.6);
     }
-#if ARV_AS241_SELECT
-    double num = central ? kAS241d[0][7] : kAS241d[2][7];
-    double den = central ? kAS241d[1][7] : kAS241d[3][7];
-#pragma unroll
-    for (int i = 6; i >= 0; --i) {
-        num = __dadd_rn(__dmul_rn(num, x), central ? kAS241d[0][i] : kAS241d[2][i]);
-        den = __dadd_rn(__dmul_rn(den, x), central ? kAS241d[1][i] : kAS241d[3][i]);
-    }
-#else
-    // per-lane coefficient row from the read-only path: one LDG per
-    // coefficient (<= 2 distinct addresses per warp, L1-resident) instead of
-    // two integer selects per coefficient
-    const double *cf = kAS241g + (central ? 0 : 16);
-    double num = __ldg(cf + 7);
-    double den = __ldg(cf + 15);
-#pragma unroll
-    for (int i = 6; i >= 0; --i) {
-        num = __dadd_rn(__dmul_rn(num, x), __ldg(cf + i));
-        den = __dadd_rn(__dmul_rn(den, x), __ldg(cf + 8 + i));
-    }
-#endif
+    double num, den;
+    as241_rational(x, central, num, den);
     const double val = __ddiv_rn(central ? __dmul_rn(q, num) : num, den);
     return central || upper ? val : -val;
 }
@@ -335,6 +359,60 @@ __device__ __forceinline__ double as241_f64_core(double u, double q, bool centra
 __device__ __forceinline__ double as241_f64(double u) {
     const double q = __dsub_rn(u, 0.5);
     return as241_f64_core(u, q, fabs(q) <= 0.425, u > 0.5);
+}
+
+// N evaluations per lane with the tail's log / sqrt compacted across the warp.
+// A warp of independent lanes almost always holds some tail value (|u - 1/2|
+// > 0.425 has probability 0.15; P(no tail among 32 lanes) = 0.5%), so
+// per-element calls run the ~100-instruction log + sqrt once per element for
+// the whole warp.  Here each pass of the loop serves the lowest pending tail
+// of every lane: passes = the largest per-lane tail count in the warp (about
+// 1.5 for N = 2 and 2.3 for N = 4 instead of N).  Every element still goes
+// through exactly the operations of as241_f64_core, so results are identical.
+template <int N>
+__device__ __forceinline__ void as241_f64_batch(const double (&u)[N], double (&out)[N]) {
+    double q[N], x[N];
+    unsigned pend = 0, central = 0, upper = 0, far = 0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        q[k] = __dsub_rn(u[k], 0.5);
+        if (fabs(q[k]) <= 0.425) central |= 1u << k;
+        else pend |= 1u << k;
+        if (u[k] > 0.5) upper |= 1u << k;
+        x[k] = __dsub_rn(0.180625, __dmul_rn(q[k], q[k]));  // central argument; tails overwrite it
+    }
+    const unsigned am = __activemask();
+    while (__any_sync(am, pend != 0u)) {
+        double w = 1.0;  // lanes without a pending tail evaluate log(1)
+        int sel = -1;
+#pragma unroll
+        for (int k = N - 1; k >= 0; --k)
+            if (pend & (1u << k)) {
+                sel = k;
+                w = (upper >> k) & 1u ? __dsub_rn(1.0, u[k]) : u[k];
+            }
+        const double r = __dsqrt_rn(-log(w));
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            if (k == sel) {
+                x[k] = __dsub_rn(r, 1.6);
+                if (r > 5.0) far |= 1u << k;
+            }
+        pend &= pend - 1u;
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const bool c = (central >> k) & 1u;
+        double num, den;
+        as241_rational(x[k], c, num, den);
+        const double val = __ddiv_rn(c ? __dmul_rn(q[k], num) : num, den);
+        out[k] = c || ((upper >> k) & 1u) ? val : -val;
+    }
+    if (far) {  // r > 5 (u < ~1.4e-11 or > 1 - 1.4e-11): E/F rational, rare
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            if ((far >> k) & 1u) out[k] = as241_f64_branchy(u[k]);
+    }
 }
 
 __device__ __forceinline__ float as241_f32_branchy(float u) {
@@ -357,8 +435,6 @@ __device__ __forceinline__ float as241_f32_branchy(float u) {
     return upper ? val : -val;
 }
 
-static __device__ const float kAS241gf[32] = {ARV_AS241_A, ARV_AS241_B, ARV_AS241_C, ARV_AS241_D};
-
 // Same results as as241_f32_branchy with one rational per lane (see as241_f64).
 __device__ __forceinline__ float as241_f32(float u) {
     const float q = __fsub_rn(u, 0.5f);
@@ -373,14 +449,8 @@ __device__ __forceinline__ float as241_f32(float u) {
         if (r > 5.0f) return as241_f32_branchy(u);
         x = __fsub_rn(r, 1.6f);
     }
-    const float *cf = kAS241gf + (central ? 0 : 16);
-    float num = __ldg(cf + 7);
-    float den = __ldg(cf + 15);
-#pragma unroll
-    for (int i = 6; i >= 0; --i) {
-        num = __fadd_rn(__fmul_rn(num, x), __ldg(cf + i));
-        den = __fadd_rn(__fmul_rn(den, x), __ldg(cf + 8 + i));
-    }
+    float num, den;
+    as241_rational(x, central, num, den);
     const float val = __fdiv_rn(central ? __fmul_rn(q, num) : num, den);
     return central || upper ? val : -val;
 }

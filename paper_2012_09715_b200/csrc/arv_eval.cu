@@ -227,9 +227,28 @@ __global__ void __launch_bounds__(kEvalBlock) k_ncchi2_eval(const double *__rest
 }
 
 // ---------------------------------------------------------- AS241 exact --
+// Four elements per thread and pass (two 16-byte vectors) so that the tail's
+// log / sqrt is compacted 4-wide across the warp (as241_f64_batch).
 __global__ void __launch_bounds__(kEvalBlock) k_gauss_inv_cdf(const double *__restrict__ u, double *__restrict__ out,
                                                               int64_t n) {
-    ew_map<false>(u, u, out, n, [](double ui) { return as241_f64(ui); });
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    int64_t head = 0;
+    if (((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+        const int64_t nq = n / 4;  // groups of 4 doubles
+        const double2 *uv = reinterpret_cast<const double2 *>(u);
+        double2 *ov = reinterpret_cast<double2 *>(out);
+        for (int64_t i = tid; i < nq; i += stride) {
+            const double2 a = __ldcs(uv + 2 * i), b = __ldcs(uv + 2 * i + 1);
+            const double x[4] = {a.x, a.y, b.x, b.y};
+            double r[4];
+            as241_f64_batch<4>(x, r);
+            __stcs(ov + 2 * i, make_double2(r[0], r[1]));
+            __stcs(ov + 2 * i + 1, make_double2(r[2], r[3]));
+        }
+        head = nq * 4;
+    }
+    for (int64_t i = head + tid; i < n; i += stride) __stcs(out + i, as241_f64(__ldcs(u + i)));
 }
 __global__ void __launch_bounds__(kEvalBlock) k_gauss_inv_cdf32(const float *__restrict__ u, float *__restrict__ out,
                                                                 int64_t n) {

@@ -25,6 +25,9 @@ namespace arv {
 
 constexpr int kLevelBlock = 256;
 // Min resident CTAs per SM (register cap) for the level kernels; see sweeps.
+#ifndef ARV_GBM_QUAD  // four-uniform passes in the Gaussian level kernels (see as241_f64_batch)
+#define ARV_GBM_QUAD 1
+#endif
 #ifndef ARV_GBM_MINB_PCG  // GBM + PCG32 instances fit 64 registers without spills (1.3% faster)
 #define ARV_GBM_MINB_PCG 4
 #endif
@@ -83,7 +86,7 @@ struct PathRng {
 
 // Compile-time uniform source of the Gaussian-scheme kernels: the PCG32 side
 // keeps the raw word, so the f64 uniform is assembled from its bits and the
-// u < 1/2 predicates are integer compares (-2% on the GBM level kernel).
+// u < 1/2 predicate is an integer compare (-2% on the GBM level kernel).
 template <bool PHILOX>
 struct PathSource;
 
@@ -95,18 +98,12 @@ struct PathSource<false> {
         const Affine jp = lcg_jump(p, A.inc);
         s = jp.a * A.s0 + jp.c;
     }
-    // exact (AS241) and table normals of the next uniform
-    template <int DEG>
-    __device__ __forceinline__ void normals(const double *tab, int64_t K1, double &z, double &a) {
+    // next uniform and the reference's u < 1/2
+    __device__ __forceinline__ double next(bool &lower) {
         const uint32_t w = pcg32_output(s);
         s = step.a * s + step.c;
-        const double u = __dsub_rn(one_plus_u32(w), 1.0);  // == u32_to_f64(w), no I2F / DMUL
-        const double q = __dsub_rn(u, 0.5);
-        // u > 1/2 <=> w >= 2^31 (integer compare instead of DSETP).  The
-        // central-region test stays in f64: as an integer compare it changes
-        // ptxas' schedule of the rare far-tail branch and spills (measured).
-        z = as241_f64_core(u, q, fabs(q) <= 0.425, w >= 0x80000000u);
-        a = gauss_table_eval<DEG>(tab, K1, u, w < 0x80000000u);
+        lower = w < 0x80000000u;  // integer compare instead of DSETP
+        return __dsub_rn(one_plus_u32(w), 1.0);  // == u32_to_f64(w), no I2F / DMUL
     }
 };
 
@@ -115,12 +112,11 @@ struct PathSource<true> {
     uint64_t s, n_paths, seed, sid;
     __device__ __forceinline__ PathSource(const LevelArgs &A, uint64_t p)
         : s(p), n_paths(A.n_paths_total), seed(A.seed), sid(A.sid) {}
-    template <int DEG>
-    __device__ __forceinline__ void normals(const double *tab, int64_t K1, double &z, double &a) {
+    __device__ __forceinline__ double next(bool &lower) {
         const double u = u64_to_f64(philox_word(s, seed, sid));  // sampler.py:62
         s += n_paths;
-        z = as241_f64(u);
-        a = gauss_table_eval<DEG>(tab, K1, u);
+        lower = u < 0.5;
+        return u;
     }
 };
 
@@ -282,20 +278,43 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
             if constexpr (GBM) return gbm_step<MIL>(x, dw, dt, A.a, A.b);
             else return cir_step<MIL>(x, dw, dt, A.a, A.b, A.c);
         };
-        for (int64_t pair = 0; pair < A.n_f / 2; ++pair) {
-            double z1, w1, z2, w2;  // exact / table normals of the same uniform
-            rng.template normals<DEG>(smd, K1, z1, w1);
-            rng.template normals<DEG>(smd, K1, z2, w2);
-            xf_e = step(step(xf_e, __dmul_rn(sq_f, z1), dt_f), __dmul_rn(sq_f, z2), dt_f);
-            xc_e = step(xc_e, __dmul_rn(sq_f, __dadd_rn(z1, z2)), dt_c);
-            xf_a = step(step(xf_a, __dmul_rn(sq_f, w1), dt_f), __dmul_rn(sq_f, w2), dt_f);
-            xc_a = step(xc_a, __dmul_rn(sq_f, __dadd_rn(w1, w2)), dt_c);
+        // one coarse step = two fine steps; exact (AS241) and table normals of
+        // the same uniforms (mlmc.py:200-229)
+        auto pair_step = [&](const double *z, const double *w) {
+            xf_e = step(step(xf_e, __dmul_rn(sq_f, z[0]), dt_f), __dmul_rn(sq_f, z[1]), dt_f);
+            xc_e = step(xc_e, __dmul_rn(sq_f, __dadd_rn(z[0], z[1])), dt_c);
+            xf_a = step(step(xf_a, __dmul_rn(sq_f, w[0]), dt_f), __dmul_rn(sq_f, w[1]), dt_f);
+            xc_a = step(xc_a, __dmul_rn(sq_f, __dadd_rn(w[0], w[1])), dt_c);
+        };
+        int64_t pairs = A.n_f / 2;
+#if ARV_GBM_QUAD
+        for (; pairs >= 2; pairs -= 2) {  // four uniforms per pass: AS241 tails compacted 4-wide
+            double u[4], z[4], w[4];
+            bool lo[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) u[k] = rng.next(lo[k]);
+            as241_f64_batch<4>(u, z);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) w[k] = gauss_table_eval<DEG>(smd, K1, u[k], lo[k]);
+            pair_step(z, w);
+            pair_step(z + 2, w + 2);
+        }
+#endif
+        for (; pairs > 0; --pairs) {
+            double u[2], z[2], w[2];
+            bool lo[2];
+            u[0] = rng.next(lo[0]);
+            u[1] = rng.next(lo[1]);
+            as241_f64_batch<2>(u, z);
+            w[0] = gauss_table_eval<DEG>(smd, K1, u[0], lo[0]);
+            w[1] = gauss_table_eval<DEG>(smd, K1, u[1], lo[1]);
+            pair_step(z, w);
         }
         if (A.n_f & 1) {
-            double z1, w1;
-            rng.template normals<DEG>(smd, K1, z1, w1);
-            xf_e = step(xf_e, __dmul_rn(sq_f, z1), dt_f);
-            xf_a = step(xf_a, __dmul_rn(sq_f, w1), dt_f);
+            bool lo;
+            const double u = rng.next(lo);
+            xf_e = step(xf_e, __dmul_rn(sq_f, as241_f64(u)), dt_f);
+            xf_a = step(xf_a, __dmul_rn(sq_f, gauss_table_eval<DEG>(smd, K1, u, lo)), dt_f);
         }
         const double fe = payoff_fn(xf_e, A.payoff, A.strike);
         const double fa = payoff_fn(xf_a, A.payoff, A.strike);

@@ -323,12 +323,13 @@ __global__ void __launch_bounds__(256) k_pcg32_gauss64(GenArgs a, double *__rest
     const Affine j0 = lcg_jump(4ull * g, a.inc);
     uint64_t s = j0.a * a.s_base + j0.c;
     for (; g < n_full; g += T) {
-        double r[4];
+        double u[4], r[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            r[i] = as241_f64(static_cast<double>(u32_to_f32(pcg32_output(s))));
+            u[i] = static_cast<double>(u32_to_f32(pcg32_output(s)));
             s = i < 3 ? lcg_step(s, kPcgMult, a.inc) : lcg_step(s, a.stride.a, a.stride.c);
         }
+        as241_f64_batch<4>(u, r);  // tail log/sqrt compacted across the warp
         double2 *o = reinterpret_cast<double2 *>(out + 4 * g);
         __stcs(o, make_double2(r[0], r[1]));
         __stcs(o + 1, make_double2(r[2], r[3]));
