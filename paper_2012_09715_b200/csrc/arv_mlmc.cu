@@ -1,8 +1,9 @@
 // Nested MLMC level kernels: one thread per path, all path states in f64
 // registers, PCG32 stream state in registers, and in-CTA two-pass reduction
-// of the per-path differences into (count, mean, M2) partials that a second
-// one-CTA kernel merges in a fixed order (Chan), so statistics are bitwise
-// reproducible for a given (path_lo, path_count) whatever the scheduling.
+// of the per-path differences into (count, mean, M2) partials, merged by a
+// second one-CTA kernel in a fixed order (parallel-axis identity), so the
+// statistics are bitwise reproducible for a given (path_lo, path_count)
+// whatever the scheduling.
 //
 // Reference loops restated (mlmc.py):
 //   GBM EM / Milstein        simulate_gbm_coupled   :164-229 (em_step :194-198)
@@ -192,63 +193,70 @@ __device__ __forceinline__ void cta_moments(const double (&d)[NK], bool valid, d
     }
 }
 
-__device__ __forceinline__ void chan_merge(double &n, double &mean, double &m2, double nb, double mb, double m2b) {
-    if (nb == 0.0) return;
-    if (n == 0.0) {
-        n = nb;
-        mean = mb;
-        m2 = m2b;
-        return;
-    }
-    const double tot = n + nb;
-    const double delta = mb - mean;
-    mean += delta * (nb / tot);
-    m2 += m2b + delta * delta * (n * nb / tot);
-    n = tot;
-}
-
-// Merge n_parts partials (n_parts x NK x 3) into out (NK x 3) in a fixed
-// order: thread t folds partials t, t + B, t + 2B, ... (coalesced), then a
-// shuffle tree within each warp and a sequential fold over the warps.
+// Merge n_parts partials (n_parts x NK x 3 of count, mean, M2) into out
+// (NK x 3) with the parallel-axis identity instead of a chain of pairwise
+// Chan merges (two divisions each):
+//   N = sum n_i,  mean = (sum n_i mean_i) / N,  M2 = sum [M2_i + n_i (mean_i - mean)^2]
+// -- two passes of plain fused multiply-adds over the partials (every M2 term
+// is non-negative), each a fixed-order block reduction (thread t takes
+// partials t, t + B, ...; xor-shuffle tree; warps summed in order), so the
+// result is bitwise reproducible.
 template <int NK>
-__global__ void __launch_bounds__(kFinalBlock) k_finalize(const double *__restrict__ parts, int64_t n_parts,
-                                                          double *__restrict__ out) {
-    __shared__ double sh[kFinalBlock / 32][NK][3];
-    double n[NK], mean[NK], m2[NK];
-#pragma unroll
-    for (int k = 0; k < NK; ++k) n[k] = mean[k] = m2[k] = 0.0;
-    for (int64_t i = threadIdx.x; i < n_parts; i += kFinalBlock) {
-        const double *p = parts + i * NK * 3;
-#pragma unroll
-        for (int k = 0; k < NK; ++k) chan_merge(n[k], mean[k], m2[k], p[3 * k], p[3 * k + 1], p[3 * k + 2]);
-    }
+__device__ __forceinline__ void block_sum(double (&v)[NK], double (*sh)[NK], double *res) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
+    for (int k = 0; k < NK; ++k) {
 #pragma unroll
-        for (int k = 0; k < NK; ++k) {
-            const double nb = __shfl_down_sync(0xffffffffu, n[k], o);
-            const double mb = __shfl_down_sync(0xffffffffu, mean[k], o);
-            const double qb = __shfl_down_sync(0xffffffffu, m2[k], o);
-            if ((lane & (2 * o - 1)) == 0) chan_merge(n[k], mean[k], m2[k], nb, mb, qb);
-        }
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < NK; ++k) {
-            sh[warp][k][0] = n[k];
-            sh[warp][k][1] = mean[k];
-            sh[warp][k][2] = m2[k];
-        }
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+        if (lane == 0) sh[warp][k] = v[k];
     }
     __syncthreads();
     if (threadIdx.x < NK) {
+        double t = 0.0;
+        for (int w = 0; w < kFinalBlock / 32; ++w) t += sh[w][threadIdx.x];
+        res[threadIdx.x] = t;
+    }
+    __syncthreads();
+}
+
+template <int NK>
+__global__ void __launch_bounds__(kFinalBlock) k_finalize(const double *__restrict__ parts, int64_t n_parts,
+                                                          double *__restrict__ out) {
+    __shared__ double sh[kFinalBlock / 32][NK];
+    __shared__ double cnt[NK], sum[NK], m2[NK];
+    double a[NK], b[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) a[k] = b[k] = 0.0;
+    for (int64_t i = threadIdx.x; i < n_parts; i += kFinalBlock) {
+        const double *p = parts + i * NK * 3;
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+            a[k] += p[3 * k];
+            b[k] = fma(p[3 * k], p[3 * k + 1], b[k]);
+        }
+    }
+    block_sum<NK>(a, sh, cnt);
+    block_sum<NK>(b, sh, sum);
+    double mean[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+        mean[k] = cnt[k] > 0.0 ? sum[k] / cnt[k] : 0.0;
+        a[k] = 0.0;
+    }
+    for (int64_t i = threadIdx.x; i < n_parts; i += kFinalBlock) {
+        const double *p = parts + i * NK * 3;
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+            const double d = p[3 * k + 1] - mean[k];
+            a[k] = fma(p[3 * k] * d, d, a[k] + p[3 * k + 2]);
+        }
+    }
+    block_sum<NK>(a, sh, m2);
+    if (threadIdx.x < NK) {
         const int k = threadIdx.x;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-        for (int w = 0; w < kFinalBlock / 32; ++w) chan_merge(a0, a1, a2, sh[w][k][0], sh[w][k][1], sh[w][k][2]);
-        out[3 * k + 0] = a0;
-        out[3 * k + 1] = a1;
-        out[3 * k + 2] = a2;
+        out[3 * k + 0] = cnt[k];
+        out[3 * k + 1] = mean[k];
+        out[3 * k + 2] = m2[k];
     }
 }
 
