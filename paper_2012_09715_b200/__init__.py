@@ -16,12 +16,14 @@ from .errors import (
     NumericalError, TableIOError, TruncatedFileError, VersionError,
 )
 from .mlmc import (
-    Allocation, CirParams, GbmParams, LevelSpec, LevelStats, estimate_level, estimate_level_suite,
-    level_stream, optimal_allocation, optimal_allocation_nested, simulate, speedup_report,
+    Allocation, CirParams, GbmParams, LevelSpec, LevelStats, PathBatch, difference, estimate_level,
+    estimate_level_suite, level_stream, optimal_allocation, optimal_allocation_nested, simulate,
+    simulate_cir_coupled, simulate_gbm_coupled, speedup_report, telescoped_mean,
 )
 from .sampler import (
-    CoupledGaussianBatch, Pcg32Stream, PhiloxStream, dyadic_index, eval_constant, eval_dyadic, eval_ncchi2,
-    eval_subdyadic, evaluate, gaussian_inv_cdf, sample_coupled, shard_range,
+    CoupledGaussianBatch, GaussianSamplePair, Pcg32Stream, PhiloxStream, UniformStream, dyadic_index,
+    eval_constant, eval_dyadic, eval_ncchi2, eval_subdyadic, evaluate, gaussian_exact_batch, gaussian_inv_cdf,
+    sample_coupled, shard_range,
 )
 from .tables import ConstantTable, DyadicPolyTable, NcChi2Table, SubDyadicTable, load_table, shipped_names
 from .tableio import export_table, import_table
@@ -29,11 +31,12 @@ from .tableio import export_table, import_table
 __all__ = [
     "ApproxRvError", "BadMagicError", "ChecksumError", "ConfigError", "DeviceError", "DomainError",
     "NumericalError", "TableIOError", "TruncatedFileError", "VersionError",
-    "Allocation", "CirParams", "GbmParams", "LevelSpec", "LevelStats", "estimate_level",
-    "estimate_level_suite", "level_stream", "optimal_allocation", "optimal_allocation_nested",
-    "simulate", "speedup_report",
-    "CoupledGaussianBatch", "Pcg32Stream", "PhiloxStream", "dyadic_index", "eval_constant", "eval_dyadic", "eval_ncchi2",
-    "eval_subdyadic", "evaluate", "gaussian_inv_cdf", "sample_coupled", "shard_range",
+    "Allocation", "CirParams", "GbmParams", "LevelSpec", "LevelStats", "PathBatch", "difference",
+    "estimate_level", "estimate_level_suite", "level_stream", "optimal_allocation", "optimal_allocation_nested",
+    "simulate", "simulate_cir_coupled", "simulate_gbm_coupled", "speedup_report", "telescoped_mean",
+    "CoupledGaussianBatch", "GaussianSamplePair", "Pcg32Stream", "PhiloxStream", "UniformStream", "dyadic_index",
+    "eval_constant", "eval_dyadic", "eval_ncchi2", "eval_subdyadic", "evaluate", "gaussian_exact_batch",
+    "gaussian_inv_cdf", "sample_coupled", "shard_range",
     "ConstantTable", "DyadicPolyTable", "NcChi2Table", "SubDyadicTable", "load_table", "shipped_names",
     "export_table", "import_table",
     "backend_name", "get_kernels",

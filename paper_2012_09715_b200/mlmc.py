@@ -276,6 +276,43 @@ def simulate(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, sides: Optional
     return PathBatch(paths[0], paths[1], paths[2], paths[3], draws_per_path=spec.n_steps_fine)
 
 
+def simulate_gbm_coupled(spec: LevelSpec, stream, n_paths: int, sides: Optional[str] = None) -> PathBatch:
+    """mlmc.py:164-229: GBM Euler-Maruyama / Milstein coupled paths."""
+    if spec.scheme not in ("euler_maruyama", "milstein"):
+        raise ConfigError(f"simulate_gbm_coupled cannot run scheme {spec.scheme!r}")
+    return simulate(spec, stream, n_paths, sides)
+
+
+def simulate_cir_coupled(spec: LevelSpec, stream, n_paths: int, sides: Optional[str] = None) -> PathBatch:
+    """mlmc.py:232-331: CIR exact / truncated Euler (and truncated Milstein) coupled paths."""
+    if spec.scheme in ("euler_maruyama", "milstein"):
+        raise ConfigError(f"simulate_cir_coupled cannot run scheme {spec.scheme!r}")
+    return simulate(spec, stream, n_paths, sides)
+
+
+def difference(spec_kind: str, rv_source, batch: PathBatch):
+    """The per-path difference a level estimates (mlmc.py:341-353), on the device."""
+    if spec_kind == "plain":
+        return batch.p_fine_exact if _is_exact(rv_source) else batch.p_fine_approx
+    if spec_kind == "two_way":
+        if _is_exact(rv_source):
+            return batch.p_fine_exact - batch.p_coarse_exact
+        return batch.p_fine_approx - batch.p_coarse_approx
+    if spec_kind != "four_way":
+        raise ConfigError(f"unknown level kind {spec_kind!r}")
+    return batch.p_fine_exact - batch.p_coarse_exact - batch.p_fine_approx + batch.p_coarse_approx
+
+
+def telescoped_mean(specs: list, seed: int, n_pilot: int, generator: str = "pcg32") -> tuple:
+    """Sum of per-level means with its combined standard error (mlmc.py:553-561)."""
+    total, var_sum = 0.0, 0.0
+    for spec in specs:
+        stats = estimate_level(spec, level_stream(seed, spec.level, generator=generator), n_pilot)
+        total += stats.mean
+        var_sum += stats.variance / stats.n_paths
+    return total, math.sqrt(var_sum)
+
+
 def _check_fail(spec, n_fail):
     if n_fail is not None:
         nf = int(n_fail.item())

@@ -178,6 +178,14 @@ def gaussian_inv_cdf(u, out=None):
 # ---------------------------------------------------------------------------
 
 @dataclass(frozen=True)
+class GaussianSamplePair:
+    """Exact and approximate Gaussian samples from one shared uniform (sampler.py:69-74)."""
+
+    z_exact: float
+    z_approx: float
+
+
+@dataclass(frozen=True)
 class CoupledGaussianBatch:
     """Arrays of coupled samples; pair i derives from the same uniform (sampler.py:77-88)."""
 
@@ -186,6 +194,9 @@ class CoupledGaussianBatch:
 
     def __len__(self) -> int:
         return int(self.z_exact.shape[0])
+
+    def __getitem__(self, i) -> GaussianSamplePair:
+        return GaussianSamplePair(float(self.z_exact[i]), float(self.z_approx[i]))
 
 
 @dataclass
@@ -460,6 +471,15 @@ def sample_coupled(stream, table, n: int) -> CoupledGaussianBatch:
     if isinstance(z_approx, torch.Tensor) and z_approx.dtype != torch.float64:
         z_approx = z_approx.to(torch.float64)
     return CoupledGaussianBatch(z_exact=z_exact, z_approx=z_approx)
+
+
+def gaussian_exact_batch(u):
+    """Exact quantile of a uniform batch (sampler.py:221-223): AS241 on the device."""
+    return gaussian_inv_cdf(u)
+
+
+# The reference's name for its Philox-4x64-10 stream (sampler.py:26-66).
+UniformStream = PhiloxStream
 
 
 def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:

@@ -209,3 +209,40 @@ def test_gbm_constant_table_source(arv, orc, tables_npz):
         s = arv.estimate_level_suite(sp, arv.level_stream(29, level), 1 << 16)
         gaps.append(math.log2(s["four_way"].variance / s["two_way_exact"].variance))
     assert -15.0 <= float(np.mean(gaps)) <= -11.0
+
+
+def test_reference_api_names(arv):
+    """mlmc.simulate_gbm_coupled / simulate_cir_coupled / difference / telescoped_mean
+    and sampler.UniformStream / GaussianSamplePair / gaussian_exact_batch under the
+    reference's names (mlmc.py:164,232,341,553; sampler.py:26,69,221)."""
+    lin = arv.load_table("dyadic_linear_k15")
+    gbm = arv.LevelSpec(level=3, scheme="euler_maruyama", process=arv.GbmParams(**GBM), rv_source=lin,
+                        kind="four_way", n0=1)
+    cir = arv.LevelSpec(level=2, scheme="cir_euler_truncated", process=arv.CirParams(**CIR), rv_source=lin,
+                        kind="four_way", n0=1)
+    b = arv.simulate_gbm_coupled(gbm, arv.level_stream(1, 3), 4096)
+    ref = arv.simulate(gbm, arv.level_stream(1, 3), 4096)
+    assert torch.equal(b.p_fine_exact, ref.p_fine_exact) and torch.equal(b.p_coarse_approx, ref.p_coarse_approx)
+    with pytest.raises(arv.ConfigError):
+        arv.simulate_gbm_coupled(cir, arv.level_stream(1, 2), 16)
+    with pytest.raises(arv.ConfigError):
+        arv.simulate_cir_coupled(gbm, arv.level_stream(1, 3), 16)
+    c = arv.simulate_cir_coupled(cir, arv.level_stream(1, 2), 1024)
+    assert c.p_fine_exact.shape[0] == 1024
+    four = arv.difference("four_way", lin, b)
+    assert torch.equal(four, b.p_fine_exact - b.p_coarse_exact - b.p_fine_approx + b.p_coarse_approx)
+    assert torch.equal(arv.difference("two_way", "exact", b), b.p_fine_exact - b.p_coarse_exact)
+    assert torch.equal(arv.difference("plain", lin, b), b.p_fine_approx)
+    specs = [arv.LevelSpec(level=lv, scheme="euler_maruyama", process=arv.GbmParams(**GBM), rv_source="exact",
+                           kind="two_way" if lv else "plain", n0=1) for lv in range(4)]
+    total, se = arv.telescoped_mean(specs, 42, 1 << 16)
+    by_hand = 0.0  # plain left-to-right sum (Python 3.12's sum() compensates)
+    for sp in specs:
+        by_hand += arv.estimate_level(sp, arv.level_stream(42, sp.level), 1 << 16).mean
+    assert total == by_hand and 0 < se < 1e-2
+    assert abs(total - math.exp(0.05)) < 6 * se
+    assert arv.UniformStream is arv.PhiloxStream
+    pair = arv.sample_coupled(arv.UniformStream(7, 1), lin, 8)[3]
+    assert isinstance(pair, arv.GaussianSamplePair)
+    u = arv.UniformStream(7, 1).uniforms(8)
+    assert pair.z_exact == float(arv.gaussian_exact_batch(u)[3])
