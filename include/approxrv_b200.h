@@ -201,6 +201,10 @@ ARV_API int arv_mlmc_cir_exact_level(const arv_level_spec *spec, const double *s
  * NULL) receives |F(x) - u| from the device CDF. */
 ARV_API int arv_ncchi2_inv_cdf(const double *u, const double *lam, int64_t nlam, double nu, const double *x0,
                        double *out, double *resid, int64_t n, void *stream);
+/* Same with the reference's `tol` (exact_dist.py:381, tol_f = min(tol, max(1e-13,
+ * 1e-4 min(u, 1-u)))); arv_ncchi2_inv_cdf is tol = 1e-9. */
+ARV_API int arv_ncchi2_inv_cdf_tol(const double *u, const double *lam, int64_t nlam, double nu, const double *x0,
+                                   double tol, double *out, double *resid, int64_t n, void *stream);
 /* Device non-central chi^2 CDF (Poisson-mixture of regularized gammas). */
 ARV_API int arv_ncchi2_cdf(const double *x, const double *lam, int64_t nlam, double nu, double *out, int64_t n,
                    void *stream);

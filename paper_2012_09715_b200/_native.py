@@ -63,6 +63,7 @@ _SIGNATURES = {
     "arv_mlmc_gaussian_level": ([C.POINTER(LevelSpec), _p, _int, _i64, _p, _p, _p, _i64, _p], _int),
     "arv_mlmc_cir_exact_level": ([C.POINTER(LevelSpec), _p, _i64, _int, _i64, _dbl, _p, _p, _p, _p, _i64, _p], _int),
     "arv_ncchi2_inv_cdf": ([_p, _p, _i64, _dbl, _p, _p, _p, _i64, _p], _int),
+    "arv_ncchi2_inv_cdf_tol": ([_p, _p, _i64, _dbl, _p, _dbl, _p, _p, _i64, _p], _int),
     "arv_ncchi2_cdf": ([_p, _p, _i64, _dbl, _p, _i64, _p], _int),
 }
 

@@ -402,11 +402,12 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(L
 // -------------------------------------------------- standalone ncchi2 --
 __global__ void __launch_bounds__(256) k_ncchi2_inv(const double *__restrict__ u, const double *__restrict__ lam,
                                                     int64_t nlam, double nu, const double *__restrict__ x0,
-                                                    double *__restrict__ out, double *__restrict__ resid, int64_t n) {
+                                                    double tol, double *__restrict__ out, double *__restrict__ resid,
+                                                    int64_t n) {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const double li = nlam == 1 ? lam[0] : lam[i];
-        const NcQuantile q = ncchi2_quantile(u[i], nu, li, x0 ? x0[i] : -1.0);
+        const NcQuantile q = ncchi2_quantile(u[i], nu, li, x0 ? x0[i] : -1.0, tol);
         out[i] = q.x;
         if (resid) resid[i] = q.resid;
     }
@@ -578,14 +579,20 @@ int arv_mlmc_cir_exact_level(const arv_level_spec *spec, const double *stacks, i
     return run_finalize(parts, nb, stats, s, "arv_mlmc_cir_exact_level(finalize)");
 }
 
-int arv_ncchi2_inv_cdf(const double *u, const double *lam, int64_t nlam, double nu, const double *x0, double *out,
-                       double *resid, int64_t n, void *stream) {
+int arv_ncchi2_inv_cdf_tol(const double *u, const double *lam, int64_t nlam, double nu, const double *x0, double tol,
+                           double *out, double *resid, int64_t n, void *stream) {
     if (!(nu > 0)) return set_error(ARV_ERR_DOMAIN, "degrees of freedom must be > 0");
+    if (!(tol > 0)) return set_error(ARV_ERR_CONFIG, "tolerance must be > 0");
     if (nlam != 1 && nlam != n) return set_error(ARV_ERR_CONFIG, "per-element lambda must match the shape of u");
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
-    k_ncchi2_inv<<<stream_grid(n, 256, 8), 256, 0, as_stream(stream)>>>(u, lam, nlam, nu, x0, out, resid, n);
+    k_ncchi2_inv<<<stream_grid(n, 256, 8), 256, 0, as_stream(stream)>>>(u, lam, nlam, nu, x0, tol, out, resid, n);
     note_launch();
     return check_launch("arv_ncchi2_inv_cdf");
+}
+
+int arv_ncchi2_inv_cdf(const double *u, const double *lam, int64_t nlam, double nu, const double *x0, double *out,
+                       double *resid, int64_t n, void *stream) {
+    return arv_ncchi2_inv_cdf_tol(u, lam, nlam, nu, x0, 1e-9, out, resid, n, stream);
 }
 
 int arv_ncchi2_cdf(const double *x, const double *lam, int64_t nlam, double nu, double *out, int64_t n, void *stream) {

@@ -186,13 +186,14 @@ struct NcQuantile {
 __device__ unsigned long long g_nc_evals, g_nc_solves;
 #endif
 
-// exact_dist.py:381-461 contract, per element, warm start x0 (<= 0: mean).
-__device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, double x0) {
+// exact_dist.py:381-461 contract, per element, warm start x0 (<= 0: mean);
+// tol is the reference's `tol` argument (default 1e-9).
+__device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, double x0, double tol = 1e-9) {
     const double a0 = 0.5 * nu;
     const double one_minus_u = 1.0 - u;
     double hi = lam + nu + 20.0 * sqrt(2.0 * (lam + nu)) + 100.0;
     double lo = 0.0;
-    const double tol_f = fmin(1e-9, fmax(1e-13, 1e-4 * fmin(u, one_minus_u)));
+    const double tol_f = fmin(tol, fmax(1e-13, 1e-4 * fmin(u, one_minus_u)));
     double x = x0 > 0.0 ? x0 : lam + nu;
     x = fmin(fmax(x, 1e-8), hi);
     const NcLam L = nc_lam(lam);

@@ -246,3 +246,37 @@ def test_reference_api_names(arv):
     assert isinstance(pair, arv.GaussianSamplePair)
     u = arv.UniformStream(7, 1).uniforms(8)
     assert pair.z_exact == float(arv.gaussian_exact_batch(u)[3])
+
+
+def test_exact_dist_module(arv):
+    """paper_2012_09715_b200.exact_dist mirrors approxrv.exact_dist on the device."""
+    from scipy import special as sp
+
+    from paper_2012_09715_b200 import exact_dist as ed
+
+    nu = 4 * 0.5 * 0.04 / 0.2**2
+    u = np.linspace(1e-6, 1 - 1e-6, 501)
+    for lam in (0.0, 3.0, 250.0):
+        x = ed.ncchi2_inv_cdf_batch(u, nu, lam)
+        assert isinstance(x, np.ndarray) and np.abs(sp.chndtr(x, nu, lam) - u).max() <= 1e-8
+        np.testing.assert_allclose(ed.ncchi2_cdf(x, nu, lam), sp.chndtr(x, nu, lam), rtol=0, atol=1e-12)
+    lam_pe = np.linspace(0.0, 400.0, u.size)
+    x = ed.ncchi2_inv_cdf_batch(u, nu, lam_pe)
+    assert np.abs(sp.chndtr(x, nu, lam_pe) - u).max() <= 1e-8
+    # looser tol: fewer Newton steps, still inside the 1e-8 contract
+    xl = ed.ncchi2_inv_cdf_batch(u, nu, 30.0, tol=1e-8)
+    assert np.abs(sp.chndtr(xl, nu, 30.0) - u).max() <= 1e-8
+    # device in, device out; scalar in, float out
+    xd = ed.ncchi2_inv_cdf_batch(torch.from_numpy(u).cuda(), nu, 3.0)
+    assert xd.is_cuda and np.array_equal(xd.cpu().numpy(), ed.ncchi2_inv_cdf_batch(u, nu, 3.0))
+    assert isinstance(ed.ncchi2_inv_cdf_batch(0.5, nu, 3.0), float)
+    with pytest.raises(arv.DomainError):
+        ed.ncchi2_inv_cdf_batch(np.array([0.0, 0.5]), nu, 1.0)
+    with pytest.raises(arv.DomainError):
+        ed.ncchi2_inv_cdf_batch(0.5, -1.0, 1.0)
+    with pytest.raises(arv.DomainError):
+        ed.ncchi2_cdf(-1.0, nu, 1.0)
+    nu_t, lam_t, scale = ed.cir_transition_params(np.array([0.04, 0.0]), 0.5, 0.04, 0.2, 0.25)
+    decay = math.exp(-0.5 * 0.25)
+    assert scale == 0.2 * 0.2 * (1.0 - decay) / (4.0 * 0.5) and nu_t == nu
+    assert np.array_equal(lam_t, np.array([0.04, 0.0]) * (decay / scale))
