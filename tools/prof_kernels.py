@@ -95,6 +95,12 @@ def main():
         sp = arv.LevelSpec(level=8, scheme="euler_maruyama", process=arv.GbmParams(0.05, 0.2, 1.0, 1.0),
                            rv_source=lin, kind="four_way", n0=1)
         res["gbm_l8"] = timed(lambda: run_level(sp, arv.level_stream(42, 8), 1 << 22), args.reps)
+    if "gbmall" in which:  # config 4: levels 0..8 x 2^22 paths, level kernel + merge each
+        lin = arv.load_table("dyadic_linear_k15")
+        sps = [arv.LevelSpec(level=lv, scheme="euler_maruyama", process=arv.GbmParams(0.05, 0.2, 1.0, 1.0),
+                             rv_source=lin, kind="four_way", n0=1) for lv in range(9)]
+        res["gbm_all"] = timed(lambda: [run_level(sp, arv.level_stream(42, sp.level), 1 << 22) for sp in sps],
+                               args.reps)
     if "cir" in which:
         tab = arv.load_table("ncchi2_cir_k64_stacks")
         sp = arv.LevelSpec(level=6, scheme="cir_exact", process=arv.CirParams(0.5, 0.04, 0.2, 0.04, 1.0),
