@@ -33,7 +33,15 @@ def require_cuda() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle(device: torch.device | None = None) -> int:
+    # torch's own fast accessor for the current cudaStream_t (~0.3 us against
+    # ~2 us for current_stream().cuda_stream, which builds a Stream object)
+    if _raw_stream is not None:
+        idx = torch.cuda.current_device() if device is None or device.index is None else device.index
+        return _raw_stream(idx)
     return torch.cuda.current_stream(device).cuda_stream
 
 
@@ -81,10 +89,12 @@ def table_on_device(arr, dtype: torch.dtype, device: torch.device | None = None)
         return to_device(arr, dtype, arr.device)
     device = device or require_cuda()
     a = np.asarray(arr)
-    key = (a.__array_interface__["data"][0], a.shape, a.dtype.str, dtype, device.index, a.flags.writeable)
     if a.flags.writeable:
         # Mutable host arrays cannot be cached safely; upload every call.
         return to_device(a, dtype, device)
+    # keyed by object identity: the entry holds `a`, so its id cannot be reused
+    # while cached, and read-only arrays never change
+    key = (id(a), dtype, device.index)
     with _table_lock:
         hit = _table_cache.get(key)
         if hit is not None and hit[0] is a:

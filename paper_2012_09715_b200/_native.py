@@ -91,8 +91,14 @@ lib = _load()
 LIB_PATH = os.environ.get("ARV_LIB_PATH") or _build.LIB_PATH
 
 
+_fns: dict = {}
+
+
 def call(name: str, *args) -> None:
-    rc = getattr(lib, name)(*args)
+    fn = _fns.get(name)
+    if fn is None:
+        fn = _fns[name] = getattr(lib, name)
+    rc = fn(*args)
     if rc:
         msg = lib.arv_last_error()
         raise_for(rc, (msg.decode() if msg else name) or name)
