@@ -345,6 +345,48 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
 }
 
 // ----------------------------------------------------------- CIR exact --
+// Lambda-sorted transitions.  The exact quantile costs ~3 sweeps whose window
+// covers ~16 sqrt(lambda/2) Poisson terms. lambda is proportional to the path
+// state, and that state spans an order of magnitude (the CIR law is
+// gamma-like). A warp therefore runs as long as its largest-lambda lane: 18-20
+// of 32 lanes were active on average. Each step, the CTA first draws the
+// uniforms, advances the approximate side and computes the table warm starts
+// in path order. It then sorts its 256 exact-side solves by lambda and hands
+// them out in sorted order, so each warp solves transitions of similar cost.
+// Results return to the owning lane through shared memory. Per-path results
+// are unchanged; only the lane that computes them differs. Sorting by the
+// predicted sweep length, which also counts the y-dependent part above the
+// window, measured 1.7% slower than sorting by lambda. The sort costs 36
+// barrier stages per step; config 5 went 68.9 -> 60.6 ms.
+#ifndef ARV_CIR_SORT
+#define ARV_CIR_SORT 1
+#endif
+
+// Ascending bitonic sort of (key, slot) over the CTA; perm[t] = slot of rank t.
+__device__ __forceinline__ void cta_sort_perm(double key, double *skey, int *perm) {
+    const int t = threadIdx.x;
+    skey[t] = key;
+    perm[t] = t;
+    __syncthreads();
+    for (int k = 2; k <= kLevelBlock; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const int o = t ^ j;
+            if (o > t) {
+                const double a = skey[t], b = skey[o];
+                const int ia = perm[t], ib = perm[o];
+                const bool gt = a > b || (a == b && ia > ib);
+                if (gt == ((t & k) == 0)) {
+                    skey[t] = b;
+                    skey[o] = a;
+                    perm[t] = ib;
+                    perm[o] = ia;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
 template <int DEG>
 __global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(LevelArgs A, const double *__restrict__ stacks,
                                                                  int64_t n_knots, int64_t K1, int use_smem,
@@ -360,26 +402,62 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(L
         __syncthreads();
         tab = st;
     }
+    // The path this thread owns: its stream, both states and fail count.  The
+    // exact solve of a step may run on another lane of the CTA (ARV_CIR_SORT).
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool valid = i < A.path_count;
-    double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if (valid) {
-        const uint64_t p = static_cast<uint64_t>(A.path_lo + i);
-        PathRng rng(A, p);
-        double x_e = A.x0, x_a = A.x0;
-        unsigned fails = 0;
-        for (int64_t k = 0; k < A.n_f; ++k) {
-            const double u = rng.next();
+    PathRng rng(A, static_cast<uint64_t>(A.path_lo + (valid ? i : 0)));
+    double x_e = A.x0, x_a = A.x0;
+    unsigned fails = 0;
+#if ARV_CIR_SORT
+    __shared__ double sh_key[kLevelBlock], sh_u[kLevelBlock], sh_lam[kLevelBlock], sh_warm[kLevelBlock];
+    __shared__ double sh_x[kLevelBlock], sh_r[kLevelBlock];
+    __shared__ int sh_perm[kLevelBlock];
+#endif
+    for (int64_t k = 0; k < A.n_f; ++k) {
+        double u = 0.5, lam_e = 0.0, warm = 0.0;
+        if (valid) {
+            u = rng.next();
             // mlmc.py:264-268 approximate side (state clamped before lambda)
             const double lam_a = __dmul_rn(fmax(x_a, 0.0), A.decay_over_scale);
             x_a = __dmul_rn(A.scale, ncchi2_eval1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_a));
             // mlmc.py:269-278 exact side, warm-started from the table
-            const double lam_e = __dmul_rn(x_e, A.decay_over_scale);
-            const double warm = ncchi2_eval1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_e);
+            lam_e = __dmul_rn(x_e, A.decay_over_scale);
+            warm = ncchi2_eval1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_e);
+        }
+#if ARV_CIR_SORT
+        const int t = threadIdx.x;
+        cta_sort_perm(valid ? lam_e : -1.0, sh_key, sh_perm);
+        sh_u[t] = u;
+        sh_lam[t] = lam_e;
+        sh_warm[t] = warm;
+        __syncthreads();
+        const int src = sh_perm[t];  // solve the transition of rank t
+        const bool solve = sh_key[t] >= 0.0;
+        double xq = 0.0, rq = 0.0;
+        if (solve) {
+            const NcQuantile q = ncchi2_quantile(sh_u[src], A.nu_exact, sh_lam[src], sh_warm[src]);
+            xq = q.x;
+            rq = q.resid;
+        }
+        sh_x[src] = xq;  // back to the owner's slot
+        sh_r[src] = rq;
+        __syncthreads();
+        if (valid) {
+            fails += sh_r[t] > 1e-8;
+            x_e = __dmul_rn(A.scale, sh_x[t]);
+        }
+        __syncthreads();
+#else
+        if (valid) {
             const NcQuantile q = ncchi2_quantile(u, A.nu_exact, lam_e, warm);
             fails += q.resid > 1e-8;
             x_e = __dmul_rn(A.scale, q.x);
         }
+#endif
+    }
+    double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (valid) {
         if (fails && n_fail) atomicAdd(n_fail, static_cast<unsigned long long>(fails));
         const double fe = payoff_fn(x_e, A.payoff, A.strike);
         const double fa = payoff_fn(x_a, A.payoff, A.strike);
@@ -606,12 +684,17 @@ int arv_ncchi2_cdf(const double *x, const double *lam, int64_t nlam, double nu, 
 
 #if ARV_NC_COUNT
 // diagnostic build only: {CDF evaluations, quantile solves} since the last call
+// out[0..1] = evaluations, solves; out[2..9] per-solve histogram; out[10..17] per-warp-max histogram
 ARV_API int arv_nc_counters(unsigned long long *out) {
     cudaMemcpyFromSymbol(out, g_nc_evals, sizeof(unsigned long long));
     cudaMemcpyFromSymbol(out + 1, g_nc_solves, sizeof(unsigned long long));
-    const unsigned long long zero = 0;
-    cudaMemcpyToSymbol(g_nc_evals, &zero, sizeof zero);
-    cudaMemcpyToSymbol(g_nc_solves, &zero, sizeof zero);
+    cudaMemcpyFromSymbol(out + 2, g_nc_hist, 8 * sizeof(unsigned long long));
+    cudaMemcpyFromSymbol(out + 10, g_nc_warp_hist, 8 * sizeof(unsigned long long));
+    const unsigned long long zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_nc_evals, zero, sizeof(unsigned long long));
+    cudaMemcpyToSymbol(g_nc_solves, zero, sizeof(unsigned long long));
+    cudaMemcpyToSymbol(g_nc_hist, zero, sizeof zero);
+    cudaMemcpyToSymbol(g_nc_warp_hist, zero, sizeof zero);
     return check_launch("arv_nc_counters");
 }
 #endif
