@@ -13,6 +13,7 @@ import glob
 import os
 import shutil
 import subprocess
+import tempfile
 import sys
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
@@ -59,8 +60,8 @@ def build(verbose_ptxas: bool = False, force: bool = False, defines=(), out: str
     if verbose_ptxas:
         common += ["-Xptxas", "-v"]
     common += [f"-D{d}" for d in defines]
-    if defines or out is not None:
-        objdir = os.path.join(objdir, os.path.basename(target))
+    if defines or out is not None:  # experiment variants: objects outside the repo
+        objdir = os.path.join(tempfile.gettempdir(), "arv_variant_build", os.path.basename(target))
         os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
