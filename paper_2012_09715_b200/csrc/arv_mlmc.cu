@@ -36,7 +36,7 @@ constexpr int kLevelBlock = 256;
 #define ARV_GBM_MINB 3
 #endif
 #ifndef ARV_CIR_MINB
-#define ARV_CIR_MINB 3
+#define ARV_CIR_MINB 4  // 64 registers (24 B spill) -> 4 CTAs/SM: 57.4 vs 60.6 ms at 3, 60.1 at 5
 #endif
 constexpr int kFinalBlock = 1024;
 
@@ -427,7 +427,9 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(L
         }
 #if ARV_CIR_SORT
         const int t = threadIdx.x;
-        cta_sort_perm(valid ? lam_e : -1.0, sh_key, sh_perm);
+        // re-sort every ARV_CIR_SORT steps; in between the permutation is
+        // reused (paths are autocorrelated, so the lambda order persists)
+        if (k % ARV_CIR_SORT == 0) cta_sort_perm(valid ? lam_e : -1.0, sh_key, sh_perm);
         sh_u[t] = u;
         sh_lam[t] = lam_e;
         sh_warm[t] = warm;
