@@ -280,3 +280,25 @@ def test_exact_dist_module(arv):
     decay = math.exp(-0.5 * 0.25)
     assert scale == 0.2 * 0.2 * (1.0 - decay) / (4.0 * 0.5) and nu_t == nu
     assert np.array_equal(lam_t, np.array([0.04, 0.0]) * (decay / scale))
+
+
+def test_cir_exact_shards_and_ragged_ctas(arv):
+    """Per-path results do not depend on which lane solved them (the CTA sorts
+    its exact-side solves by lambda) nor on how paths are sharded: one launch of
+    700 paths equals shards [0, 130) + [130, 700) bit for bit (ragged CTAs)."""
+    from paper_2012_09715_b200.mlmc import run_level
+
+    tab = arv.load_table("ncchi2_cir_k64_stacks")
+    spec = arv.LevelSpec(level=4, scheme="cir_exact", process=arv.CirParams(**CIR), rv_source=tab,
+                         kind="four_way", n0=1)
+    n = 700
+    _, full, nf = run_level(spec, arv.level_stream(9, 4), n, want_paths=True)
+    assert nf is None or int(nf.item()) == 0
+    _, a, _ = run_level(spec, arv.level_stream(9, 4), n, path_lo=0, path_count=130, want_paths=True)
+    _, b, _ = run_level(spec, arv.level_stream(9, 4), n, path_lo=130, path_count=570, want_paths=True)
+    both = torch.cat([a, b], dim=1)
+    assert torch.equal(bits_t(full), bits_t(both))
+
+
+def bits_t(t):
+    return t.contiguous().view(torch.int64)
