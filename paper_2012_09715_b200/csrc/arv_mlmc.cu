@@ -480,16 +480,36 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(L
 }
 
 // -------------------------------------------------- standalone ncchi2 --
-__global__ void __launch_bounds__(256) k_ncchi2_inv(const double *__restrict__ u, const double *__restrict__ lam,
-                                                    int64_t nlam, double nu, const double *__restrict__ x0,
-                                                    double tol, double *__restrict__ out, double *__restrict__ resid,
-                                                    int64_t n) {
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const double li = nlam == 1 ? lam[0] : lam[i];
-        const NcQuantile q = ncchi2_quantile(u[i], nu, li, x0 ? x0[i] : -1.0, tol);
-        out[i] = q.x;
-        if (resid) resid[i] = q.resid;
+// Per-element lambda: tiles of 256 elements are solved in lambda order (the
+// sort of the CIR level kernel) so that a warp's lanes have similar window
+// lengths; a shared lambda needs no sort.
+__global__ void __launch_bounds__(kLevelBlock) k_ncchi2_inv(const double *__restrict__ u, const double *__restrict__ lam,
+                                                            int64_t nlam, double nu, const double *__restrict__ x0,
+                                                            double tol, double *__restrict__ out,
+                                                            double *__restrict__ resid, int64_t n) {
+    if (nlam == 1) {
+        const double l0 = lam[0];
+        for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const NcQuantile q = ncchi2_quantile(u[i], nu, l0, x0 ? x0[i] : -1.0, tol);
+            out[i] = q.x;
+            if (resid) resid[i] = q.resid;
+        }
+        return;
+    }
+    __shared__ double sh_key[kLevelBlock];
+    __shared__ int sh_perm[kLevelBlock];
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * kLevelBlock; base < n;
+         base += static_cast<int64_t>(gridDim.x) * kLevelBlock) {  // CTA-uniform tile loop
+        const int64_t mine = base + threadIdx.x;
+        cta_sort_perm(mine < n ? lam[mine] : -1.0, sh_key, sh_perm);
+        const int64_t i = base + sh_perm[threadIdx.x];  // element of rank t (tail slots sort first)
+        if (i < n) {
+            const NcQuantile q = ncchi2_quantile(u[i], nu, lam[i], x0 ? x0[i] : -1.0, tol);
+            out[i] = q.x;
+            if (resid) resid[i] = q.resid;
+        }
+        __syncthreads();  // sh_key / sh_perm reused by the next tile
     }
 }
 __global__ void __launch_bounds__(256) k_ncchi2_cdf(const double *__restrict__ x, const double *__restrict__ lam,
@@ -665,7 +685,8 @@ int arv_ncchi2_inv_cdf_tol(const double *u, const double *lam, int64_t nlam, dou
     if (!(tol > 0)) return set_error(ARV_ERR_CONFIG, "tolerance must be > 0");
     if (nlam != 1 && nlam != n) return set_error(ARV_ERR_CONFIG, "per-element lambda must match the shape of u");
     if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
-    k_ncchi2_inv<<<stream_grid(n, 256, 8), 256, 0, as_stream(stream)>>>(u, lam, nlam, nu, x0, tol, out, resid, n);
+    k_ncchi2_inv<<<stream_grid(n, kLevelBlock, 8), kLevelBlock, 0, as_stream(stream)>>>(u, lam, nlam, nu, x0, tol, out,
+                                                                                       resid, n);
     note_launch();
     return check_launch("arv_ncchi2_inv_cdf");
 }
