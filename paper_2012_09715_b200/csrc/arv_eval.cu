@@ -210,7 +210,10 @@ __device__ __forceinline__ void ncchi2_map(const double *tab, int64_t n_knots, i
 }
 
 template <int DEG>
-__global__ void __launch_bounds__(kEvalBlock) k_ncchi2_eval(const double *__restrict__ stacks, int64_t n_knots,
+// Linear tables (the shipped ones): 64 registers, 4 CTAs/SM (20 B spill) --
+// more bytes in flight: shared-lambda 0.96 -> 0.87 ms at 2^28.  Higher
+// degrees keep the ~80-register, 3-CTA shape.
+__global__ void __launch_bounds__(kEvalBlock, DEG == 1 ? 4 : 3) k_ncchi2_eval(const double *__restrict__ stacks, int64_t n_knots,
                                                             int64_t K1, int use_smem, double nu,
                                                             const double *__restrict__ u,
                                                             const double *__restrict__ lam, int64_t nlam,
