@@ -80,6 +80,14 @@ __device__ __forceinline__ uint64_t pack2(uint32_t lo, uint32_t hi) {
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
     return r;
 }
+// Float pair as one f32x2 register.  Written with float operands so that
+// ptxas can fold per-half sign / abs modifiers into the consuming FADD2
+// (-|x| costs nothing there, where an integer sign OR is a LOP3 per lane).
+__device__ __forceinline__ uint64_t pack2f(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
 __device__ __forceinline__ uint32_t lo32(uint64_t x) { return static_cast<uint32_t>(x); }
 __device__ __forceinline__ uint32_t hi32(uint64_t x) { return static_cast<uint32_t>(x >> 32); }
 __device__ __forceinline__ uint64_t f32x2_add(uint64_t a, uint64_t b) {

@@ -219,9 +219,9 @@ struct EvalSubDyadic {
     int shift;
     uint32_t four;  // 4, held in a register so the address is one IMAD (FMA pipe)
     __device__ __forceinline__ uint32_t operator()(uint32_t w) const {
-        const float f = __uint_as_float(0x3F000000u | (w >> 9));
-        const float d = __fmaf_rn(2.0f, __fadd_rn(f, -0.75f), 0x1p-24f);  // exact
-        const float v = __fadd_rn(0.5f, -fabsf(d));                       // exact
+        const float f = __uint_as_float(0x3F800000u | (w >> 9));        // 1 + u - 2^-24, in [1, 2)
+        const float d = __fadd_rn(__fadd_rn(f, -1.5f), 0x1p-24f);       // u - 1/2, exact
+        const float v = __fadd_rn(0.5f, -fabsf(d));                     // 1/2 - |u - 1/2|, exact
         const uint32_t addr = mad_u32(__float_as_uint(v) >> shift, four, base);
         float z = lds_f32<DEG * kLatticePlane * 4>(addr);
 #pragma unroll
@@ -245,10 +245,13 @@ struct EvalSubDyadic {
     // and the sum still separately rounded), so results are bit-identical.
     static constexpr bool kHasPair = DEG == 1;
     __device__ __forceinline__ void pair(uint32_t w0, uint32_t w1, uint32_t &r0, uint32_t &r1) const {
-        const uint64_t f = pack2(0x3F000000u | (w0 >> 9), 0x3F000000u | (w1 >> 9));
-        const uint64_t d = f32x2_fma(kTwo2, f32x2_add(f, kMinus075x2), kUlp24x2);  // u - 1/2, exact
+        // f = 1 + u - 2^-24 from the word's bits; d = (f - 3/2) + 2^-24 = u - 1/2
+        // and v = 1/2 - |d| are exact: three FADD2 with immediate operands,
+        // the -|d| folded into the last one as an operand modifier.
+        const uint64_t f = pack2(0x3F800000u | (w0 >> 9), 0x3F800000u | (w1 >> 9));
+        const uint64_t d = f32x2_add(f32x2_add(f, kMinus15x2), kUlp24x2);
         const uint32_t d0 = lo32(d), d1 = hi32(d);
-        const uint64_t v = f32x2_add(kHalf2, pack2(d0 | 0x80000000u, d1 | 0x80000000u));  // 1/2 - |d|, exact
+        const uint64_t v = f32x2_add(kHalf2, pack2f(-fabsf(__uint_as_float(d0)), -fabsf(__uint_as_float(d1))));
         const uint32_t a0 = mad_u32(lo32(v) >> shift, four, base);
         const uint32_t a1 = mad_u32(hi32(v) >> shift, four, base);
         const uint64_t c1 = pack2(__float_as_uint(lds_f32<kLatticePlane * 4>(a0)),
@@ -263,8 +266,7 @@ struct EvalSubDyadic {
         r0 = __float_as_uint(z0) ^ (~d0 & 0x80000000u);
         r1 = __float_as_uint(z1) ^ (~d1 & 0x80000000u);
     }
-    static constexpr uint64_t kTwo2 = 0x4000000040000000ull;       // {2, 2}
-    static constexpr uint64_t kMinus075x2 = 0xBF400000BF400000ull;  // {-0.75, -0.75}
+    static constexpr uint64_t kMinus15x2 = 0xBFC00000BFC00000ull;   // {-1.5, -1.5}
     static constexpr uint64_t kUlp24x2 = 0x3380000033800000ull;     // {2^-24, 2^-24}
     static constexpr uint64_t kHalf2 = 0x3F0000003F000000ull;       // {0.5, 0.5}
 };
