@@ -104,6 +104,10 @@ def test_device_ncchi2_quantile_contract(arv, nu):
         resid = np.abs(sp.chndtr(x, nu, lam) - u)
         assert resid.max() <= 1e-8, (lam, resid.max(), u[np.argmax(resid)])
         assert rd.cpu().numpy().max() <= 1e-8
+        # bulk solves (7-sigma sweep) still meet tol_f = 1e-9 against CDFLIB, up to
+        # the reference's own 5e-12 series-vs-CDFLIB allowance
+        bulk = (u >= 1e-6) & (u <= 1 - 1e-6)
+        assert resid[bulk].max() <= 1e-9 + 5e-12, (lam, resid[bulk].max())
 
 
 @pytest.mark.parametrize("nu", [4 * 0.5 * 0.04 / 0.2**2, 1.0, 7.3])
