@@ -92,7 +92,8 @@ __device__ inline double nc_logdens(double x, double m) {
 
 struct NcCdf {
     double resid;  // F(x) - u
-    double pdf;
+    double pdf;    // f(x) = S_1 / 2
+    double s0;     // S_0 = sum_j Pois(j; h) G(a0 + j, y): the density of nu + 2, times 2
 };
 
 // Half-width of the Poisson window and height of the gamma sweep above y, in
@@ -131,8 +132,13 @@ __device__ inline NcLam nc_lam(double lam, double sigmas = kNcSigmas) {
     return L;
 }
 
-// F(x) - u and f(x) for x > 0, a0 = nu / 2.
-__device__ inline NcCdf ncchi2_cdf_minus(double a0, double x, const NcLam &L, double u) {
+// F(x) - u for x > 0, a0 = nu / 2.  FULL: also the density f(x) = S_1 / 2,
+// S_0 (for the Taylor step) and the Poisson normaliser 1 / sum_window p_j,
+// returned in inv_w.  !FULL (a verification evaluation of the same solve):
+// F only, normalised by the caller's inv_w -- 7 instead of 10 FP64
+// operations per window term.
+template <bool FULL>
+__device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, double u, double &inv_w) {
     const double y = 0.5 * x;
     const int top = L.top, bot = L.bot;
     const int jy = static_cast<int>(ceil(y - a0)) + static_cast<int>(L.sigmas * sqrt(y)) + 10;
@@ -159,23 +165,26 @@ __device__ inline NcCdf ncchi2_cdf_minus(double a0, double x, const NcLam &L, do
     if (L.h > 0.0) {
         const double inv_h = L.inv_h;
         double p = L.p_top;
-        double wsum = 0.0, acc = 0.0, dens = 0.0;
+        double wsum = 0.0, acc = 0.0, dens = 0.0, s0 = 0.0;
         for (int i = top; i > j && i >= bot; --i) {  // window indices whose gamma terms underflowed
-            wsum += p;
+            if constexpr (FULL) wsum += p;
             p *= static_cast<double>(i) * inv_h;
         }
         for (; j >= bot; --j) {
-            wsum += p;
             acc = fma(p, P, acc);
             const double Gm = G * fma(jd, inv_y, a0y);  // G(a0 + j - 1)
-            dens = fma(p, Gm, dens);
+            if constexpr (FULL) {
+                wsum += p;
+                s0 = fma(p, G, s0);
+                dens = fma(p, Gm, dens);
+            }
             P += Gm;
             G = Gm;
             p *= jd * inv_h;
             jd -= 1.0;
         }
-        const double inv_w = 1.0 / wsum;
-        return {fma(acc, inv_w, -u), 0.5 * dens * inv_w};
+        if constexpr (FULL) inv_w = 1.0 / wsum;
+        return {fma(acc, inv_w, -u), 0.5 * dens * inv_w, s0 * inv_w};
     }
     // h == 0: the central law, F = P(a0, y), f = G(a0 - 1, y) / 2
     for (; j > 0; --j) {
@@ -183,7 +192,12 @@ __device__ inline NcCdf ncchi2_cdf_minus(double a0, double x, const NcLam &L, do
         P += G;
         jd -= 1.0;
     }
-    return {P - u, 0.5 * G * a0y};
+    return {P - u, 0.5 * G * a0y, G};
+}
+
+__device__ inline NcCdf ncchi2_cdf_minus(double a0, double x, const NcLam &L, double u) {
+    double inv_w;
+    return ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w);
 }
 
 struct NcQuantile {
@@ -194,6 +208,62 @@ struct NcQuantile {
 #ifndef ARV_NC_HALLEY
 #define ARV_NC_HALLEY 1
 #endif
+// Degree of the Taylor-polynomial step (0: Newton / Halley steps instead).
+#ifndef ARV_NC_TAYLOR
+#define ARV_NC_TAYLOR 4
+#endif
+
+// One high-order step from a CDF evaluation.  With y = x/2 and
+// S_k = sum_j Pois(j; h) G(a0 + j - k, y) (S_k is twice the density of
+// nu - 2k + 2 degrees of freedom), d/dy F = S_1 and d/dy S_k = S_{k+1} - S_k,
+// so the n-th y-derivative of F is the forward difference Delta^{n-1} S_1.
+// The S_k obey the Bessel recurrence in the order
+//     S_{k+1} = (h S_{k-1} + (a0 - k) S_k) / y        (I_{m-1} - I_{m+1} = 2m/z I_m,
+// stable in this direction), so the sweep's S_0 and S_1 give every Taylor
+// coefficient of F around x for a few FP64 operations.  The step is the root
+// of the degree-DEG Taylor polynomial nearest 0 (Newton on the polynomial from
+// the plain Newton step, registers only).  From the table warm start its
+// error is ~(warm-start error)^(DEG+1): for config 5 (DEG = 4), 99.99% of
+// solves meet tol_f after this one step, so a solve costs 2 CDF evaluations
+// (start + verification) instead of the 2.98 of Newton / Halley steps
+// (tools/nc_diag.py).  DEG 4 / 5 / 6 measured 22.9 / 23.4 / 23.5 ms at
+// level 6.  Returns the x-step, or NaN.
+template <int DEG>
+__device__ inline double nc_taylor_step(const NcCdf &c, double a0, double h, double x) {
+    const double inv_y = 2.0 / x;
+    double D[DEG];
+    double sm = c.s0, sk = 2.0 * c.pdf;  // S_{k-1}, S_k
+    D[0] = sk;
+#pragma unroll
+    for (int k = 1; k < DEG; ++k) {
+        const double sn = fma(h, sm, (a0 - static_cast<double>(k)) * sk) * inv_y;
+        sm = sk;
+        sk = sn;
+        D[k] = sk;
+    }
+    double cf[DEG + 1];
+    cf[0] = c.resid;
+    double fact = 1.0;
+#pragma unroll
+    for (int n = 1; n <= DEG; ++n) {
+        fact *= static_cast<double>(n);
+        cf[n] = D[0] / fact;
+#pragma unroll
+        for (int i = 0; i < DEG - n; ++i) D[i] = D[i + 1] - D[i];
+    }
+    double d = -c.resid / cf[1];
+#pragma unroll
+    for (int it = 0; it < 3; ++it) {
+        double p = cf[DEG], dp = 0.0;
+#pragma unroll
+        for (int n = DEG - 1; n >= 0; --n) {
+            dp = fma(dp, d, p);
+            p = fma(p, d, cf[n]);
+        }
+        d -= p / dp;
+    }
+    return 2.0 * d;
+}
 
 #if ARV_NC_COUNT  // diagnostic build: CDF evaluations per solve, per lane and per warp (max)
 __device__ unsigned long long g_nc_evals, g_nc_solves, g_nc_hist[8], g_nc_warp_hist[8];
@@ -216,19 +286,25 @@ __device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, do
     double x = x0 > 0.0 ? x0 : lam + nu;
     x = fmin(fmax(x, 1e-8), hi);
     const NcLam L = nc_lam(lam, fmin(u, one_minus_u) >= 1e-6 ? kNcSigmasBulk : kNcSigmas);
-    NcCdf c = ncchi2_cdf_minus(a0, x, L, u);
+    double inv_w;
+    NcCdf c = ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w);
 #if ARV_NC_COUNT
     int n_eval = 1;
 #endif
-#if ARV_NC_HALLEY
+#if ARV_NC_HALLEY && !ARV_NC_TAYLOR
     double x_prev = 0.0, pdf_prev = 0.0;
 #endif
     for (int it = 0; it < 80; ++it) {
         if (fabs(c.resid) <= tol_f) break;
         if (c.resid > 0.0) hi = x;
         else lo = x;
+#if ARV_NC_TAYLOR
+        double dx = -nc_taylor_step<ARV_NC_TAYLOR>(c, a0, L.h, x);
+        if (!isfinite(dx)) dx = c.resid / c.pdf;  // Newton
+#else
         double dx = c.resid / c.pdf;  // Newton
-#if ARV_NC_HALLEY
+#endif
+#if ARV_NC_HALLEY && !ARV_NC_TAYLOR
         if (it > 0 && x != x_prev) {
             // Halley with the density slope from the last two iterates (a free
             // secant estimate of F''): near-cubic second step, so far fewer
@@ -244,7 +320,14 @@ __device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, do
         double xn = x - dx;
         if (!isfinite(xn) || xn <= lo || xn >= hi) xn = 0.5 * (lo + hi);
         x = xn;
-        c = ncchi2_cdf_minus(a0, x, L, u);
+#if ARV_NC_TAYLOR
+        // Verify the step with the F-only sweep; only a failed step (0.01%
+        // of solves) needs the derivatives at the new point for another one.
+        c = ncchi2_cdf_sweep<false>(a0, x, L, u, inv_w);
+        if (fabs(c.resid) > tol_f) c = ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w);
+#else
+        c = ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w);
+#endif
 #if ARV_NC_COUNT
         ++n_eval;
 #endif
