@@ -25,6 +25,12 @@
 namespace arv {
 
 constexpr int kLevelBlock = 256;
+// CTA size of the CIR exact level kernel (its lambda sort spans the CTA).
+#ifndef ARV_CIR_BLOCK
+#define ARV_CIR_BLOCK 256
+#endif
+constexpr int kCirBlock = ARV_CIR_BLOCK;
+constexpr int kMinLevelBlock = kCirBlock < kLevelBlock ? kCirBlock : kLevelBlock;
 // Min resident CTAs per SM (register cap) for the level kernels; see sweeps.
 #ifndef ARV_GBM_QUAD  // four-uniform passes in the Gaussian level kernels (see as241_f64_batch)
 #define ARV_GBM_QUAD 1
@@ -145,9 +151,9 @@ __device__ __forceinline__ double cir_step(double x, double dw, double dt, doubl
 
 // ------------------------------------------------------ CTA reduction --
 // Two-pass (count, mean, M2) of NK values per thread over the CTA.
-template <int NK>
+template <int NK, int BS = kLevelBlock>
 __device__ __forceinline__ void cta_moments(const double (&d)[NK], bool valid, double *partial_out) {
-    __shared__ double red[NK][kLevelBlock / 32];
+    __shared__ double red[NK][BS / 32];
     __shared__ double mean_sh[NK];
     __shared__ int cnt_sh;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -167,7 +173,7 @@ __device__ __forceinline__ void cta_moments(const double (&d)[NK], bool valid, d
     const int count = cnt_sh;
     if (threadIdx.x < NK) {
         double t = 0.0;
-        for (int w = 0; w < kLevelBlock / 32; ++w) t += red[threadIdx.x][w];
+        for (int w = 0; w < BS / 32; ++w) t += red[threadIdx.x][w];
         mean_sh[threadIdx.x] = count > 0 ? t / count : 0.0;
     }
     __syncthreads();
@@ -185,7 +191,7 @@ __device__ __forceinline__ void cta_moments(const double (&d)[NK], bool valid, d
     __syncthreads();
     if (threadIdx.x < NK) {
         double t = 0.0;
-        for (int w = 0; w < kLevelBlock / 32; ++w) t += red[threadIdx.x][w];
+        for (int w = 0; w < BS / 32; ++w) t += red[threadIdx.x][w];
         double *o = partial_out + 3 * threadIdx.x;
         o[0] = count;
         o[1] = mean_sh[threadIdx.x];
@@ -363,12 +369,13 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
 #endif
 
 // Ascending bitonic sort of (key, slot) over the CTA; perm[t] = slot of rank t.
+template <int BS>
 __device__ __forceinline__ void cta_sort_perm(double key, double *skey, int *perm) {
     const int t = threadIdx.x;
     skey[t] = key;
     perm[t] = t;
     __syncthreads();
-    for (int k = 2; k <= kLevelBlock; k <<= 1) {
+    for (int k = 2; k <= BS; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             const int o = t ^ j;
             if (o > t) {
@@ -388,7 +395,7 @@ __device__ __forceinline__ void cta_sort_perm(double key, double *skey, int *per
 }
 
 template <int DEG>
-__global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(LevelArgs A, const double *__restrict__ stacks,
+__global__ void __launch_bounds__(kCirBlock, ARV_CIR_MINB) k_cir_exact_level(LevelArgs A, const double *__restrict__ stacks,
                                                                  int64_t n_knots, int64_t K1, int use_smem,
                                                                  double *__restrict__ parts,
                                                                  double *__restrict__ paths,
@@ -410,9 +417,9 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(L
     double x_e = A.x0, x_a = A.x0;
     unsigned fails = 0;
 #if ARV_CIR_SORT
-    __shared__ double sh_key[kLevelBlock], sh_u[kLevelBlock], sh_lam[kLevelBlock], sh_warm[kLevelBlock];
-    __shared__ double sh_x[kLevelBlock], sh_r[kLevelBlock];
-    __shared__ int sh_perm[kLevelBlock];
+    __shared__ double sh_key[kCirBlock], sh_u[kCirBlock], sh_lam[kCirBlock], sh_warm[kCirBlock];
+    __shared__ double sh_x[kCirBlock], sh_r[kCirBlock];
+    __shared__ int sh_perm[kCirBlock];
 #endif
     for (int64_t k = 0; k < A.n_f; ++k) {
         double u = 0.5, lam_e = 0.0, warm = 0.0;
@@ -429,7 +436,7 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(L
         const int t = threadIdx.x;
         // re-sort every ARV_CIR_SORT steps; in between the permutation is
         // reused (paths are autocorrelated, so the lambda order persists)
-        if (k % ARV_CIR_SORT == 0) cta_sort_perm(valid ? lam_e : -1.0, sh_key, sh_perm);
+        if (k % ARV_CIR_SORT == 0) cta_sort_perm<kCirBlock>(valid ? lam_e : -1.0, sh_key, sh_perm);
         sh_u[t] = u;
         sh_lam[t] = lam_e;
         sh_warm[t] = warm;
@@ -476,7 +483,7 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_CIR_MINB) k_cir_exact_level(L
             paths[3 * A.path_count + i] = fa;
         }
     }
-    cta_moments<ARV_NKIND>(d, valid, parts + static_cast<int64_t>(blockIdx.x) * 3 * ARV_NKIND);
+    cta_moments<ARV_NKIND, kCirBlock>(d, valid, parts + static_cast<int64_t>(blockIdx.x) * 3 * ARV_NKIND);
 }
 
 // -------------------------------------------------- standalone ncchi2 --
@@ -502,7 +509,7 @@ __global__ void __launch_bounds__(kLevelBlock) k_ncchi2_inv(const double *__rest
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * kLevelBlock; base < n;
          base += static_cast<int64_t>(gridDim.x) * kLevelBlock) {  // CTA-uniform tile loop
         const int64_t mine = base + threadIdx.x;
-        cta_sort_perm(mine < n ? lam[mine] : -1.0, sh_key, sh_perm);
+        cta_sort_perm<kLevelBlock>(mine < n ? lam[mine] : -1.0, sh_key, sh_perm);
         const int64_t i = base + sh_perm[threadIdx.x];  // element of rank t (tail slots sort first)
         if (i < n) {
             const NcQuantile q = ncchi2_quantile(u[i], nu, lam[i], x0 ? x0[i] : -1.0, tol);
@@ -559,7 +566,7 @@ static int fill_common(const arv_level_spec *sp, LevelArgs &A) {
     return ARV_OK;
 }
 
-static int64_t n_blocks_for(int64_t count) { return (count + kLevelBlock - 1) / kLevelBlock; }
+static int64_t n_blocks_for(int64_t count, int bs = kLevelBlock) { return (count + bs - 1) / bs; }
 
 static int run_finalize(double *parts, int64_t nb, double *stats, cudaStream_t s, const char *what) {
     k_finalize<ARV_NKIND><<<1, kFinalBlock, 0, s>>>(parts, nb, stats);
@@ -574,7 +581,7 @@ using namespace arv;
 extern "C" {
 
 int64_t arv_mlmc_workspace_bytes(int64_t path_count) {
-    const int64_t nb = n_blocks_for(path_count < 1 ? 1 : path_count);
+    const int64_t nb = n_blocks_for(path_count < 1 ? 1 : path_count, kMinLevelBlock);
     return nb * 3 * ARV_NKIND * static_cast<int64_t>(sizeof(double));
 }
 
@@ -650,7 +657,7 @@ int arv_mlmc_cir_exact_level(const arv_level_spec *spec, const double *stacks, i
     A.nu_exact = 4.0 * kappa * theta / (sigma * sigma);
     A.decay_over_scale = std::exp(-kappa * dt) / A.scale;
     A.nu_table = nu;
-    const int64_t nb = n_blocks_for(spec->path_count);
+    const int64_t nb = n_blocks_for(spec->path_count, kCirBlock);
     if (workspace_bytes < nb * 3 * ARV_NKIND * static_cast<int64_t>(sizeof(double)))
         return set_error(ARV_ERR_CONFIG, "workspace too small");
     double *parts = static_cast<double *>(workspace);
@@ -663,7 +670,7 @@ int arv_mlmc_cir_exact_level(const arv_level_spec *spec, const double *stacks, i
     case D:                                                                                                  \
         if (smem > 40 * 1024)                                                                                \
             cudaFuncSetAttribute(k_cir_exact_level<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        k_cir_exact_level<D><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, stacks, n_knots, K1, use_smem, parts, paths, nf); \
+        k_cir_exact_level<D><<<(unsigned)nb, kCirBlock, smem, s>>>(A, stacks, n_knots, K1, use_smem, parts, paths, nf); \
         break;
     switch (degree) {
         ARV_CASE(1)
