@@ -391,7 +391,10 @@ __device__ __forceinline__ void as241_f64_batch(const double (&u)[N], double (&o
     }
     const unsigned am = __activemask();
     while (__any_sync(am, pend != 0u)) {
-        double w = 1.0;  // lanes without a pending tail evaluate log(1)
+        // Lanes without a pending tail evaluate a dummy log(1/2): with w = 1 the
+        // sqrt argument would be -0, which sends the whole warp through
+        // __dsqrt_rn's out-of-range slow path on every pass.
+        double w = 0.5;
         int sel = -1;
 #pragma unroll
         for (int k = N - 1; k >= 0; --k)
