@@ -134,6 +134,9 @@ ARV_API int arv_store_probe_ex(float *out, int64_t n, int mode, void *stream);
  * kernel's resident count, fewer when n is small (>= 64 samples per thread). */
 #define ARV_TUNE_GROUP 1
 #define ARV_TUNE_CTAS_PER_SM 2
+/* ARV_TUNE_CIR_SEGMENT = steps per segment of a CIR exact level (default 4;
+ * 0 = one kernel per level); see arv_mlmc_cir_workspace_bytes. */
+#define ARV_TUNE_CIR_SEGMENT 3
 ARV_API int arv_set_tuning(int key, int value);
 
 /* ---- nested MLMC level kernels ------------------------------------------
@@ -178,6 +181,11 @@ typedef struct {
 } arv_level_spec;
 
 ARV_API int64_t arv_mlmc_workspace_bytes(int64_t path_count);
+/* Workspace for arv_mlmc_cir_exact_level's segmented mode (paths re-bucketed
+ * by lambda across the grid between segments of ARV_TUNE_CIR_SEGMENT steps;
+ * ~84 B per path).  With only arv_mlmc_workspace_bytes the level runs as one
+ * kernel.  Results are identical either way. */
+ARV_API int64_t arv_mlmc_cir_workspace_bytes(int64_t path_count);
 
 /* GBM (euler_maruyama / milstein, mlmc.py:164-229) and CIR truncated Euler
  * (mlmc.py:289-331) / truncated Milstein (new).  table: Gaussian dyadic

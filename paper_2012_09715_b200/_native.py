@@ -60,6 +60,7 @@ _SIGNATURES = {
     "arv_store_probe_ex": ([_p, _i64, _int, _p], _int),
     "arv_set_tuning": ([_int, _int], _int),
     "arv_mlmc_workspace_bytes": ([_i64], _i64),
+    "arv_mlmc_cir_workspace_bytes": ([_i64], _i64),
     "arv_mlmc_gaussian_level": ([C.POINTER(LevelSpec), _p, _int, _i64, _p, _p, _p, _i64, _p], _int),
     "arv_mlmc_cir_exact_level": ([C.POINTER(LevelSpec), _p, _i64, _int, _i64, _dbl, _p, _p, _p, _p, _i64, _p], _int),
     "arv_ncchi2_inv_cdf": ([_p, _p, _i64, _dbl, _p, _p, _p, _i64, _p], _int),

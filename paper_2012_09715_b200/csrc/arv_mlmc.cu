@@ -69,9 +69,12 @@ struct PathRng {
     Affine step;
     uint64_t n_paths, seed, sid;
     int philox;
-    __device__ __forceinline__ PathRng(const LevelArgs &A, uint64_t p)
+    // state: a stored stream position (segmented CIR levels), else path p's start
+    __device__ __forceinline__ PathRng(const LevelArgs &A, uint64_t p, const uint64_t *state = nullptr)
         : step(A.step), n_paths(A.n_paths_total), seed(A.seed), sid(A.sid), philox(A.rng == ARV_RNG_PHILOX) {
-        if (philox) {
+        if (state) {
+            s = *state;
+        } else if (philox) {
             s = p;
         } else {
             const Affine jp = lcg_jump(p, A.inc);
@@ -363,10 +366,10 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
 // are unchanged; only the lane that computes them differs. Sorting by the
 // predicted sweep length, which also counts the y-dependent part above the
 // window, measured 1.7% slower than sorting by lambda. The sort costs 36
-// barrier stages per step; config 5 went 68.9 -> 60.6 ms.
-#ifndef ARV_CIR_SORT
-#define ARV_CIR_SORT 1
-#endif
+// barrier stages per step; config 5 went 68.9 -> 60.6 ms.  Since the
+// segmented form below keeps every CTA's lambdas close (grid-wide buckets),
+// the per-step sort is only used by the one-kernel form of long levels
+// (the SORT instantiation); short levels (<= 8 steps) run faster without it.
 
 // Ascending bitonic sort of (key, slot) over the CTA; perm[t] = slot of rank t.
 template <int BS>
@@ -394,12 +397,43 @@ __device__ __forceinline__ void cta_sort_perm(double key, double *skey, int *per
     }
 }
 
-template <int DEG>
+// Segmented mode (long levels): the level runs as segments of a few steps.
+// Between segments the paths are bucketed by lambda over the whole grid
+// (counting sort on the float exponent + 3 mantissa bits of lambda, ~9%
+// wide buckets), so every CTA holds paths of similar lambda: its warps then
+// carry similar sweep lengths and the post-solve barrier stops waiting on
+// one heavy warp (28% of warp stall samples in the one-kernel form).  Each
+// path's state (both sides, stream position, fail count, path id) travels
+// with it in a slot-indexed record; per-path results are unchanged, and the
+// statistics are reduced afterwards in path order by the same CTA partition,
+// so they are bitwise identical to the one-kernel form.
+struct CirSeg {
+    int64_t k0, nsteps;
+    int first, last;
+    const double *xe_in, *xa_in;
+    const uint64_t *rs_in;
+    const uint32_t *fl_in, *pid_in;
+    double *xe_out, *xa_out;
+    uint64_t *rs_out;
+    uint32_t *fl_out, *pid_out;
+    uint32_t *bucket;  // !last: lambda bucket of each slot's next step
+    uint32_t *hist;    // !last: global bucket counts (zeroed by the caller)
+    double *pay;       // last (segmented): pay[pid] = p_exact, pay[n + pid] = p_approx
+};
+constexpr int kCirBuckets = 256;
+
+__device__ __forceinline__ uint32_t cir_bucket(double lam) {
+    // lambda in [2^-8, 2^24) -> 8 buckets per octave; clamped outside
+    const int b = static_cast<int>(__float_as_uint(static_cast<float>(lam)) >> 20) - ((127 - 8) << 3);
+    return static_cast<uint32_t>(b < 0 ? 0 : (b >= kCirBuckets ? kCirBuckets - 1 : b));
+}
+
+template <int DEG, bool SORT>
 __global__ void __launch_bounds__(kCirBlock, ARV_CIR_MINB) k_cir_exact_level(LevelArgs A, const double *__restrict__ stacks,
                                                                  int64_t n_knots, int64_t K1, int use_smem,
                                                                  double *__restrict__ parts,
                                                                  double *__restrict__ paths,
-                                                                 unsigned long long *__restrict__ n_fail) {
+                                                                 unsigned long long *__restrict__ n_fail, CirSeg G) {
     extern __shared__ double smd[];
     const double *tab = stacks;
     if (use_smem) {
@@ -409,19 +443,25 @@ __global__ void __launch_bounds__(kCirBlock, ARV_CIR_MINB) k_cir_exact_level(Lev
         __syncthreads();
         tab = st;
     }
-    // The path this thread owns: its stream, both states and fail count.  The
-    // exact solve of a step may run on another lane of the CTA (ARV_CIR_SORT).
+    // The path this thread owns (slot i): its stream, both states and fail
+    // count.  The exact solve of a step may run on another lane of the CTA
+    // (the SORT instantiation).
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool valid = i < A.path_count;
-    PathRng rng(A, static_cast<uint64_t>(A.path_lo + (valid ? i : 0)));
+    uint32_t pid = static_cast<uint32_t>(valid ? i : 0);
     double x_e = A.x0, x_a = A.x0;
     unsigned fails = 0;
-#if ARV_CIR_SORT
-    __shared__ double sh_key[kCirBlock], sh_u[kCirBlock], sh_lam[kCirBlock], sh_warm[kCirBlock];
-    __shared__ double sh_x[kCirBlock], sh_r[kCirBlock];
-    __shared__ int sh_perm[kCirBlock];
-#endif
-    for (int64_t k = 0; k < A.n_f; ++k) {
+    if (!G.first && valid) {
+        pid = G.pid_in[i];
+        x_e = G.xe_in[i];
+        x_a = G.xa_in[i];
+        fails = G.fl_in[i];
+    }
+    PathRng rng(A, static_cast<uint64_t>(A.path_lo + pid), G.first || !valid ? nullptr : G.rs_in + i);
+    __shared__ double sh_key[SORT ? kCirBlock : 1], sh_u[SORT ? kCirBlock : 1], sh_lam[SORT ? kCirBlock : 1],
+        sh_warm[SORT ? kCirBlock : 1], sh_x[SORT ? kCirBlock : 1], sh_r[SORT ? kCirBlock : 1];
+    __shared__ int sh_perm[SORT ? kCirBlock : 1];
+    for (int64_t k = 0; k < G.nsteps; ++k) {
         double u = 0.5, lam_e = 0.0, warm = 0.0;
         if (valid) {
             u = rng.next();
@@ -432,44 +472,66 @@ __global__ void __launch_bounds__(kCirBlock, ARV_CIR_MINB) k_cir_exact_level(Lev
             lam_e = __dmul_rn(x_e, A.decay_over_scale);
             warm = ncchi2_eval1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_e);
         }
-#if ARV_CIR_SORT
-        const int t = threadIdx.x;
-        // re-sort every ARV_CIR_SORT steps; in between the permutation is
-        // reused (paths are autocorrelated, so the lambda order persists)
-        if (k % ARV_CIR_SORT == 0) cta_sort_perm<kCirBlock>(valid ? lam_e : -1.0, sh_key, sh_perm);
-        sh_u[t] = u;
-        sh_lam[t] = lam_e;
-        sh_warm[t] = warm;
-        __syncthreads();
-        const int src = sh_perm[t];  // solve the transition of rank t
-        const bool solve = sh_key[t] >= 0.0;
-        double xq = 0.0, rq = 0.0;
-        if (solve) {
-            const NcQuantile q = ncchi2_quantile(sh_u[src], A.nu_exact, sh_lam[src], sh_warm[src]);
-            xq = q.x;
-            rq = q.resid;
-        }
-        sh_x[src] = xq;  // back to the owner's slot
-        sh_r[src] = rq;
-        __syncthreads();
-        if (valid) {
-            fails += sh_r[t] > 1e-8;
-            x_e = __dmul_rn(A.scale, sh_x[t]);
-        }
-        __syncthreads();
-#else
-        if (valid) {
+        if constexpr (SORT) {
+            const int t = threadIdx.x;
+            cta_sort_perm<kCirBlock>(valid ? lam_e : -1.0, sh_key, sh_perm);
+            sh_u[t] = u;
+            sh_lam[t] = lam_e;
+            sh_warm[t] = warm;
+            __syncthreads();
+            const int src = sh_perm[t];  // solve the transition of rank t
+            const bool solve = sh_key[t] >= 0.0;
+            double xq = 0.0, rq = 0.0;
+            if (solve) {
+                const NcQuantile q = ncchi2_quantile(sh_u[src], A.nu_exact, sh_lam[src], sh_warm[src]);
+                xq = q.x;
+                rq = q.resid;
+            }
+            sh_x[src] = xq;  // back to the owner's slot
+            sh_r[src] = rq;
+            __syncthreads();
+            if (valid) {
+                fails += sh_r[t] > 1e-8;
+                x_e = __dmul_rn(A.scale, sh_x[t]);
+            }
+            __syncthreads();
+        } else if (valid) {
             const NcQuantile q = ncchi2_quantile(u, A.nu_exact, lam_e, warm);
             fails += q.resid > 1e-8;
             x_e = __dmul_rn(A.scale, q.x);
         }
-#endif
+    }
+    if (!G.last) {  // hand the record on and count its next-step lambda bucket
+        __shared__ uint32_t hist[kCirBuckets];
+        for (int b = threadIdx.x; b < kCirBuckets; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        if (valid) {
+            G.xe_out[i] = x_e;
+            G.xa_out[i] = x_a;
+            G.rs_out[i] = rng.s;
+            G.fl_out[i] = fails;
+            G.pid_out[i] = pid;
+            const uint32_t b = cir_bucket(__dmul_rn(x_e, A.decay_over_scale));
+            G.bucket[i] = b;
+            atomicAdd(&hist[b], 1u);
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < kCirBuckets; b += blockDim.x)
+            if (hist[b]) atomicAdd(&G.hist[b], hist[b]);
+        return;
+    }
+    const double fe = payoff_fn(x_e, A.payoff, A.strike);
+    const double fa = payoff_fn(x_a, A.payoff, A.strike);
+    if (valid && fails && n_fail) atomicAdd(n_fail, static_cast<unsigned long long>(fails));
+    if (!G.first) {  // segmented: payoffs by path id, reduced in path order afterwards
+        if (valid) {
+            G.pay[pid] = fe;
+            G.pay[A.path_count + pid] = fa;
+        }
+        return;
     }
     double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (valid) {
-        if (fails && n_fail) atomicAdd(n_fail, static_cast<unsigned long long>(fails));
-        const double fe = payoff_fn(x_e, A.payoff, A.strike);
-        const double fa = payoff_fn(x_a, A.payoff, A.strike);
         // coarse slots repeat the fine payoffs (mlmc.py:281-286), so both
         // two-way differences vanish; slot 2 carries the exact - approx
         // correction of reproduce.py:299-301, slots 3/4 the process values.
@@ -479,6 +541,80 @@ __global__ void __launch_bounds__(kCirBlock, ARV_CIR_MINB) k_cir_exact_level(Lev
         if (paths) {
             paths[i] = fe;
             paths[A.path_count + i] = fe;  // coarse slots repeat fine (mlmc.py:281-286)
+            paths[2 * A.path_count + i] = fa;
+            paths[3 * A.path_count + i] = fa;
+        }
+    }
+    cta_moments<ARV_NKIND, kCirBlock>(d, valid, parts + static_cast<int64_t>(blockIdx.x) * 3 * ARV_NKIND);
+}
+
+// Exclusive scan of the bucket counts into per-bucket cursors; clears the
+// counts for the next segment.  One CTA of kCirBuckets threads.
+__global__ void __launch_bounds__(kCirBuckets) k_cir_bucket_scan(uint32_t *hist, uint32_t *cursor) {
+    __shared__ uint32_t sh[kCirBuckets];
+    const int t = threadIdx.x;
+    const uint32_t v = hist[t];
+    sh[t] = v;
+    __syncthreads();
+    for (int o = 1; o < kCirBuckets; o <<= 1) {  // Hillis-Steele inclusive scan
+        const uint32_t add = t >= o ? sh[t - o] : 0u;
+        __syncthreads();
+        sh[t] += add;
+        __syncthreads();
+    }
+    cursor[t] = sh[t] - v;
+    hist[t] = 0;
+}
+
+// Move each record to its bucket's range (a CTA reserves one contiguous run
+// per bucket it holds; order inside a bucket is immaterial to the results).
+__global__ void __launch_bounds__(kCirBlock) k_cir_scatter(int64_t n, const uint32_t *__restrict__ bucket,
+                                                           uint32_t *cursor, const double *__restrict__ xe,
+                                                           const double *__restrict__ xa,
+                                                           const uint64_t *__restrict__ rs,
+                                                           const uint32_t *__restrict__ fl,
+                                                           const uint32_t *__restrict__ pid, double *xe_o,
+                                                           double *xa_o, uint64_t *rs_o, uint32_t *fl_o,
+                                                           uint32_t *pid_o) {
+    __shared__ uint32_t cnt[kCirBuckets], base[kCirBuckets];
+    for (int b = threadIdx.x; b < kCirBuckets; b += blockDim.x) cnt[b] = 0;
+    __syncthreads();
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint32_t b = 0, local = 0;
+    if (i < n) {
+        b = bucket[i];
+        local = atomicAdd(&cnt[b], 1u);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < kCirBuckets; c += blockDim.x)
+        if (cnt[c]) base[c] = atomicAdd(&cursor[c], cnt[c]);
+    __syncthreads();
+    if (i < n) {
+        const uint32_t dst = base[b] + local;
+        xe_o[dst] = xe[i];
+        xa_o[dst] = xa[i];
+        rs_o[dst] = rs[i];
+        fl_o[dst] = fl[i];
+        pid_o[dst] = pid[i];
+    }
+}
+
+// Statistics of a segmented level, in path order with the one-kernel CTA
+// partition (bitwise identical to it).
+__global__ void __launch_bounds__(kCirBlock) k_cir_payoff_moments(LevelArgs A, const double *__restrict__ pay,
+                                                                  double *__restrict__ parts,
+                                                                  double *__restrict__ paths) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool valid = i < A.path_count;
+    double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (valid) {
+        const double fe = pay[i], fa = pay[A.path_count + i];
+        d[2] = __dsub_rn(fe, fa);
+        d[3] = fe;
+        d[4] = fa;
+        if (paths) {
+            paths[i] = fe;
+            paths[A.path_count + i] = fe;
             paths[2 * A.path_count + i] = fa;
             paths[3 * A.path_count + i] = fa;
         }
@@ -574,6 +710,41 @@ static int run_finalize(double *parts, int64_t nb, double *stats, cudaStream_t s
     return check_launch(what);
 }
 
+// Steps per segment of a segmented CIR exact level (0: always one kernel);
+// arv_set_tuning(ARV_TUNE_CIR_SEGMENT).
+int g_cir_segment = 4;
+
+static int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
+
+// Workspace of a segmented CIR exact level: CTA partials, two record
+// buffers (slot-indexed SoA), buckets, bucket counts / cursors, payoffs.
+struct CirWs {
+    int64_t total = 0;
+    double *parts = nullptr, *xe[2] = {}, *xa[2] = {}, *pay = nullptr;
+    uint64_t *rs[2] = {};
+    uint32_t *fl[2] = {}, *pid[2] = {}, *bucket = nullptr, *hist = nullptr, *cursor = nullptr;
+    CirWs(int64_t n, void *base) {
+        char *p = static_cast<char *>(base);
+        auto take = [&](int64_t bytes) -> void * {
+            void *r = p ? p + total : nullptr;
+            total += align256(bytes);
+            return r;
+        };
+        parts = static_cast<double *>(take(n_blocks_for(n, kCirBlock) * 3 * ARV_NKIND * int64_t(sizeof(double))));
+        for (int b = 0; b < 2; ++b) {
+            xe[b] = static_cast<double *>(take(8 * n));
+            xa[b] = static_cast<double *>(take(8 * n));
+            rs[b] = static_cast<uint64_t *>(take(8 * n));
+            fl[b] = static_cast<uint32_t *>(take(4 * n));
+            pid[b] = static_cast<uint32_t *>(take(4 * n));
+        }
+        bucket = static_cast<uint32_t *>(take(4 * n));
+        hist = static_cast<uint32_t *>(take(4 * kCirBuckets));
+        cursor = static_cast<uint32_t *>(take(4 * kCirBuckets));
+        pay = static_cast<double *>(take(16 * n));
+    }
+};
+
 }  // namespace arv
 
 using namespace arv;
@@ -583,6 +754,10 @@ extern "C" {
 int64_t arv_mlmc_workspace_bytes(int64_t path_count) {
     const int64_t nb = n_blocks_for(path_count < 1 ? 1 : path_count, kMinLevelBlock);
     return nb * 3 * ARV_NKIND * static_cast<int64_t>(sizeof(double));
+}
+
+int64_t arv_mlmc_cir_workspace_bytes(int64_t path_count) {
+    return CirWs(path_count < 1 ? 1 : path_count, nullptr).total;
 }
 
 int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, int degree, int64_t K1, double *stats,
@@ -657,32 +832,84 @@ int arv_mlmc_cir_exact_level(const arv_level_spec *spec, const double *stacks, i
     A.nu_exact = 4.0 * kappa * theta / (sigma * sigma);
     A.decay_over_scale = std::exp(-kappa * dt) / A.scale;
     A.nu_table = nu;
-    const int64_t nb = n_blocks_for(spec->path_count, kCirBlock);
+    const int64_t n = spec->path_count;
+    const int64_t nb = n_blocks_for(n, kCirBlock);
     if (workspace_bytes < nb * 3 * ARV_NKIND * static_cast<int64_t>(sizeof(double)))
         return set_error(ARV_ERR_CONFIG, "workspace too small");
-    double *parts = static_cast<double *>(workspace);
     const size_t bytes = sizeof(double) * 2 * n_knots * (degree + 1) * K1;
     const int use_smem = bytes <= 128 * 1024;
     const size_t smem = use_smem ? bytes : 0;
     cudaStream_t s = as_stream(stream);
     unsigned long long *nf = reinterpret_cast<unsigned long long *>(n_fail);
-#define ARV_CASE(D)                                                                                          \
-    case D:                                                                                                  \
-        if (smem > 40 * 1024)                                                                                \
-            cudaFuncSetAttribute(k_cir_exact_level<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        k_cir_exact_level<D><<<(unsigned)nb, kCirBlock, smem, s>>>(A, stacks, n_knots, K1, use_smem, parts, paths, nf); \
-        break;
+    // Segmented when the level is longer than one segment, the path ids fit
+    // 32 bits and the caller's workspace holds the records.
+    const int64_t seg = g_cir_segment;
+    const bool segmented = seg > 0 && A.n_f > seg && n < (int64_t(1) << 32) &&
+                           workspace_bytes >= CirWs(n, nullptr).total;
+    const CirWs W(n, workspace);
+    double *parts = segmented ? W.parts : static_cast<double *>(workspace);
+    // CTA lambda sort per step: only for the one-kernel form of long levels
+    const bool sort = !segmented && A.n_f > 8;
+    const void *fn = nullptr;
+#define ARV_PICK(D) fn = sort ? (const void *)k_cir_exact_level<D, true> : (const void *)k_cir_exact_level<D, false>
     switch (degree) {
-        ARV_CASE(1)
-        ARV_CASE(2)
-        ARV_CASE(3)
-        ARV_CASE(4)
-        ARV_CASE(5)
+        case 1: ARV_PICK(1); break;
+        case 2: ARV_PICK(2); break;
+        case 3: ARV_PICK(3); break;
+        case 4: ARV_PICK(4); break;
+        case 5: ARV_PICK(5); break;
         default: return set_error(ARV_ERR_CONFIG, "polynomial degree must be in [1, 5], got %d", degree);
     }
-#undef ARV_CASE
+#undef ARV_PICK
+    if (smem > 40 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto launch = [&](const CirSeg &G) {
+        void *args[] = {(void *)&A, (void *)&stacks, (void *)&n_knots, (void *)&K1, (void *)&use_smem,
+                        (void *)&parts, (void *)&paths, (void *)&nf, (void *)&G};
+        cudaLaunchKernel(fn, dim3((unsigned)nb), dim3(kCirBlock), args, smem, s);
+        note_launch();
+    };
+    if (!segmented) {
+        CirSeg G{};
+        G.k0 = 0;
+        G.nsteps = A.n_f;
+        G.first = G.last = 1;
+        launch(G);
+        if (int rc = check_launch("arv_mlmc_cir_exact_level")) return rc;
+        return run_finalize(parts, nb, stats, s, "arv_mlmc_cir_exact_level(finalize)");
+    }
+    cudaMemsetAsync(W.hist, 0, 4 * kCirBuckets, s);
+    for (int64_t k0 = 0; k0 < A.n_f; k0 += seg) {
+        CirSeg G{};
+        G.k0 = k0;
+        G.nsteps = A.n_f - k0 < seg ? A.n_f - k0 : seg;
+        G.first = k0 == 0;
+        G.last = k0 + G.nsteps >= A.n_f;
+        G.xe_in = W.xe[0];
+        G.xa_in = W.xa[0];
+        G.rs_in = W.rs[0];
+        G.fl_in = W.fl[0];
+        G.pid_in = W.pid[0];
+        G.xe_out = W.xe[1];
+        G.xa_out = W.xa[1];
+        G.rs_out = W.rs[1];
+        G.fl_out = W.fl[1];
+        G.pid_out = W.pid[1];
+        G.bucket = W.bucket;
+        G.hist = W.hist;
+        G.pay = W.pay;
+        launch(G);
+        if (int rc = check_launch("arv_mlmc_cir_exact_level(segment)")) return rc;
+        if (G.last) break;
+        k_cir_bucket_scan<<<1, kCirBuckets, 0, s>>>(W.hist, W.cursor);
+        note_launch();
+        k_cir_scatter<<<(unsigned)nb, kCirBlock, 0, s>>>(n, W.bucket, W.cursor, W.xe[1], W.xa[1], W.rs[1], W.fl[1],
+                                                          W.pid[1], W.xe[0], W.xa[0], W.rs[0], W.fl[0], W.pid[0]);
+        note_launch();
+        if (int rc = check_launch("arv_mlmc_cir_exact_level(rebucket)")) return rc;
+    }
+    k_cir_payoff_moments<<<(unsigned)nb, kCirBlock, 0, s>>>(A, W.pay, parts, paths);
     note_launch();
-    if (int rc = check_launch("arv_mlmc_cir_exact_level")) return rc;
+    if (int rc = check_launch("arv_mlmc_cir_exact_level(moments)")) return rc;
     return run_finalize(parts, nb, stats, s, "arv_mlmc_cir_exact_level(finalize)");
 }
 

@@ -35,6 +35,7 @@ constexpr int kGenUnroll = ARV_GEN_UNROLL;
 // Process-wide launch shape knobs (arv_set_tuning); defaults from sweeps.
 static int g_group = 8;        // samples per thread-group: 4 (v4) or 8 (v8)
 static int g_ctas_per_sm = 0;  // CTAs per SM (256 threads each); 0 = auto (see gen_grid)
+extern int g_cir_segment;      // arv_mlmc.cu
 
 constexpr int kJumpBits = 24;  // grid threads < 2^24
 
@@ -437,6 +438,10 @@ int arv_set_tuning(int key, int value) {
         case ARV_TUNE_GROUP:
             if (value != 4 && value != 8) return set_error(ARV_ERR_CONFIG, "group must be 4 or 8");
             g_group = value;
+            return ARV_OK;
+        case ARV_TUNE_CIR_SEGMENT:
+            if (value < 0) return set_error(ARV_ERR_CONFIG, "cir segment must be >= 0");
+            g_cir_segment = value;
             return ARV_OK;
         case ARV_TUNE_CTAS_PER_SM:
             if (value < 0 || value > 32) return set_error(ARV_ERR_CONFIG, "ctas_per_sm must be in [0 (auto), 32]");

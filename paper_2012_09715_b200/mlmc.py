@@ -251,7 +251,8 @@ def run_level(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, *, path_lo: in
     ns = _native_spec(spec, stream, n_paths, path_lo, count)
     stats = torch.empty(NSLOT * 3, dtype=torch.float64, device=device)
     paths = torch.empty((4, count), dtype=torch.float64, device=device) if want_paths else None
-    ws_bytes = int(nat.lib.arv_mlmc_workspace_bytes(count))
+    ws_fn = nat.lib.arv_mlmc_cir_workspace_bytes if spec.scheme == "cir_exact" else nat.lib.arv_mlmc_workspace_bytes
+    ws_bytes = int(ws_fn(count))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
     s = dev.stream_handle(device)
     pp = paths.data_ptr() if paths is not None else None

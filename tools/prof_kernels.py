@@ -58,7 +58,10 @@ def main():
     ap.add_argument("--group", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--cirseg", type=int, default=-1, help="CIR exact steps per segment (0: one kernel)")
     args = ap.parse_args()
+    if args.cirseg >= 0:
+        _native.call("arv_set_tuning", 3, args.cirseg)
     if args.group:
         _native.call("arv_set_tuning", 1, args.group)
     if args.ctas:
