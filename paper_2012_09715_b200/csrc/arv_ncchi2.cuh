@@ -132,11 +132,17 @@ __device__ inline NcLam nc_lam(double lam, double sigmas = kNcSigmas) {
     return L;
 }
 
-// F(x) - u for x > 0, a0 = nu / 2.  FULL: also the density f(x) = S_1 / 2,
-// S_0 (for the Taylor step) and the Poisson normaliser 1 / sum_window p_j,
-// returned in inv_w.  !FULL (a verification evaluation of the same solve):
-// F only, normalised by the caller's inv_w -- 7 instead of 10 FP64
-// operations per window term.
+// F(x) - u for x > 0, a0 = nu / 2.  FULL: also the density f(x) = S_1 / 2
+// and S_0 (for the Taylor step).  !FULL (a verification evaluation of the
+// same solve): F only -- 7 instead of 9 FP64 operations per window term.
+// The Poisson weights are not renormalised by their window sum
+// (ARV_NC_NORMALISE=0): p_top is Loader's saddle-point pmf (a few ulp), the
+// window drops < 1e-15 of the Poisson mass, and the downward recurrence
+// drifts by ~(window length) ulp, so F moves by < 1e-13 and one FP64
+// operation per term is saved.
+#ifndef ARV_NC_NORMALISE
+#define ARV_NC_NORMALISE 0
+#endif
 template <bool FULL>
 __device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, double u, double &inv_w) {
     const double y = 0.5 * x;
@@ -167,14 +173,14 @@ __device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, do
         double p = L.p_top;
         double wsum = 0.0, acc = 0.0, dens = 0.0, s0 = 0.0;
         for (int i = top; i > j && i >= bot; --i) {  // window indices whose gamma terms underflowed
-            if constexpr (FULL) wsum += p;
+            if constexpr (FULL && ARV_NC_NORMALISE) wsum += p;
             p *= static_cast<double>(i) * inv_h;
         }
         for (; j >= bot; --j) {
             acc = fma(p, P, acc);
             const double Gm = G * fma(jd, inv_y, a0y);  // G(a0 + j - 1)
             if constexpr (FULL) {
-                wsum += p;
+                if constexpr (ARV_NC_NORMALISE) wsum += p;
                 s0 = fma(p, G, s0);
                 dens = fma(p, Gm, dens);
             }
@@ -183,7 +189,7 @@ __device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, do
             p *= jd * inv_h;
             jd -= 1.0;
         }
-        if constexpr (FULL) inv_w = 1.0 / wsum;
+        if constexpr (FULL) inv_w = ARV_NC_NORMALISE ? 1.0 / wsum : 1.0;
         return {fma(acc, inv_w, -u), 0.5 * dens * inv_w, s0 * inv_w};
     }
     // h == 0: the central law, F = P(a0, y), f = G(a0 - 1, y) / 2
