@@ -373,11 +373,22 @@ __device__ __forceinline__ double as241_f64(double u) {
 // A warp of independent lanes almost always holds some tail value (|u - 1/2|
 // > 0.425 has probability 0.15; P(no tail among 32 lanes) = 0.5%), so
 // per-element calls run the ~100-instruction log + sqrt once per element for
-// the whole warp.  Here each pass of the loop serves the lowest pending tail
-// of every lane: passes = the largest per-lane tail count in the warp (about
-// 1.5 for N = 2 and 2.3 for N = 4 instead of N).  Every element still goes
-// through exactly the operations of as241_f64_core, so results are identical.
-template <int N>
+// the whole warp.  Here the warp's pending tails are compacted through a
+// per-warp shared-memory list and served 32 at a time: one log + sqrt pass per
+// 32 tails of the warp (0.6 per 4 uniforms on average, so one pass for
+// nearly every N = 4 batch).  The earlier per-lane form (ARV_AS241_SMEM_COMPACT
+// = 0) served the lowest pending tail of every lane per pass: as many passes
+// as the busiest lane has tails (about 1.5 for N = 2 and 2.3 for N = 4).
+// Every element still goes through exactly the operations of
+// as241_f64_core, so results are identical.
+// LIST selects the shared-memory list (GBM level kernels: 19.9 -> 17.6 ms for
+// config 4); the standalone AS241 kernels keep the per-lane passes, which
+// measured 2% faster there (0.996 vs 1.014 ms for gauss64).
+#ifndef ARV_AS241_SMEM_COMPACT
+#define ARV_AS241_SMEM_COMPACT 1
+#endif
+constexpr int kTailWarps = 8;  // callers launch <= 256 threads per CTA
+template <int N, bool LIST = false>
 __device__ __forceinline__ void as241_f64_batch(const double (&u)[N], double (&out)[N]) {
     double q[N], x[N];
     unsigned pend = 0, central = 0, upper = 0, far = 0;
@@ -390,6 +401,41 @@ __device__ __forceinline__ void as241_f64_batch(const double (&u)[N], double (&o
         x[k] = __dsub_rn(0.180625, __dmul_rn(q[k], q[k]));  // central argument; tails overwrite it
     }
     const unsigned am = __activemask();
+    if constexpr (LIST && ARV_AS241_SMEM_COMPACT) {
+    // Every pending tail of the warp goes to a per-warp shared-memory list;
+    // the active lanes take its entries round-robin (one log + sqrt per
+    // 32 tails instead of one per busiest lane's tail) and the results return
+    // through the same slots.  Same operations per element.
+    static_assert(N <= 4, "tail buffer holds 4 elements per lane");
+    __shared__ double tail_buf[kTailWarps][32 * 4];
+    double *buf = tail_buf[threadIdx.x >> 5];
+    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+    int pos[N];
+    int total = 0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const unsigned b = __ballot_sync(am, (pend >> k) & 1u);
+        pos[k] = total + __popc(b & lt);
+        total += __popc(b);
+    }
+    if (total) {  // warp-uniform
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            if ((pend >> k) & 1u) buf[pos[k]] = (upper >> k) & 1u ? __dsub_rn(1.0, u[k]) : u[k];
+        __syncwarp(am);
+        const int na = __popc(am);
+        for (int g = __popc(am & lt); g < total; g += na) buf[g] = __dsqrt_rn(-log(buf[g]));
+        __syncwarp(am);
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            if ((pend >> k) & 1u) {
+                const double r = buf[pos[k]];
+                x[k] = __dsub_rn(r, 1.6);
+                if (r > 5.0) far |= 1u << k;
+            }
+        __syncwarp(am);  // the list is reused by the next call
+    }
+    } else {
     while (__any_sync(am, pend != 0u)) {
         // Lanes without a pending tail evaluate a dummy log(1/2): with w = 1 the
         // sqrt argument would be -0, which sends the whole warp through
@@ -410,6 +456,7 @@ __device__ __forceinline__ void as241_f64_batch(const double (&u)[N], double (&o
                 if (r > 5.0) far |= 1u << k;
             }
         pend &= pend - 1u;
+    }
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) {

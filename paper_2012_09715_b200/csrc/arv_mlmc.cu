@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
             bool lo[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) u[k] = rng.next(lo[k]);
-            as241_f64_batch<4>(u, z);
+            as241_f64_batch<4, true>(u, z);
 #pragma unroll
             for (int k = 0; k < 4; ++k) w[k] = gauss_table_eval<DEG>(smd, K1, u[k], lo[k]);
             pair_step(z, w);
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
             bool lo[2];
             u[0] = rng.next(lo[0]);
             u[1] = rng.next(lo[1]);
-            as241_f64_batch<2>(u, z);
+            as241_f64_batch<2, true>(u, z);
             w[0] = gauss_table_eval<DEG>(smd, K1, u[0], lo[0]);
             w[1] = gauss_table_eval<DEG>(smd, K1, u[1], lo[1]);
             pair_step(z, w);
