@@ -277,7 +277,23 @@ static __device__ const AS241Pairs<float> kAS241pf = as241_pairs<float>();
 
 // num(x) / den(x) of the lane's rational (central A/B or near-tail C/D),
 // Horner with separately rounded multiply and add in the reference's order.
-__device__ __forceinline__ void as241_rational(double x, bool central, double &num, double &den) {
+// rows: the 16 (A_i, B_i) / (C_i, D_i) pairs staged in shared memory by the
+// caller (as241_stage_rows), or nullptr to read them through the read-only path.
+__device__ __forceinline__ void as241_rational(double x, bool central, double &num, double &den,
+                                               const double2 *rows = nullptr) {
+    if (rows) {
+        const double2 *cf = rows + (central ? 0 : 8);
+        double2 c = cf[7];
+        num = c.x;
+        den = c.y;
+#pragma unroll
+        for (int i = 6; i >= 0; --i) {
+            c = cf[i];
+            num = __dadd_rn(__dmul_rn(num, x), c.x);
+            den = __dadd_rn(__dmul_rn(den, x), c.y);
+        }
+        return;
+    }
     const double2 *cf = reinterpret_cast<const double2 *>(kAS241pd.v) + (central ? 0 : 8);
     double2 c = __ldg(cf + 7);
     num = c.x;
@@ -288,6 +304,11 @@ __device__ __forceinline__ void as241_rational(double x, bool central, double &n
         num = __dadd_rn(__dmul_rn(num, x), c.x);
         den = __dadd_rn(__dmul_rn(den, x), c.y);
     }
+}
+// Copy the AS241 coefficient pairs to shared memory (16 double2; the caller
+// synchronises the CTA before use).
+__device__ __forceinline__ void as241_stage_rows(double2 *rows) {
+    if (threadIdx.x < 16) rows[threadIdx.x] = reinterpret_cast<const double2 *>(kAS241pd.v)[threadIdx.x];
 }
 __device__ __forceinline__ void as241_rational(float x, bool central, float &num, float &den) {
     const float2 *cf = reinterpret_cast<const float2 *>(kAS241pf.v) + (central ? 0 : 8);
@@ -389,7 +410,8 @@ __device__ __forceinline__ double as241_f64(double u) {
 #endif
 constexpr int kTailWarps = 8;  // callers launch <= 256 threads per CTA
 template <int N, bool LIST = false>
-__device__ __forceinline__ void as241_f64_batch(const double (&u)[N], double (&out)[N]) {
+__device__ __forceinline__ void as241_f64_batch(const double (&u)[N], double (&out)[N],
+                                                const double2 *rows = nullptr) {
     double q[N], x[N];
     unsigned pend = 0, central = 0, upper = 0, far = 0;
 #pragma unroll
@@ -462,7 +484,7 @@ __device__ __forceinline__ void as241_f64_batch(const double (&u)[N], double (&o
     for (int k = 0; k < N; ++k) {
         const bool c = (central >> k) & 1u;
         double num, den;
-        as241_rational(x[k], c, num, den);
+        as241_rational(x[k], c, num, den, rows);
         const double val = __ddiv_rn(c ? __dmul_rn(q[k], num) : num, den);
         out[k] = c || ((upper >> k) & 1u) ? val : -val;
     }

@@ -35,6 +35,9 @@ constexpr int kMinLevelBlock = kCirBlock < kLevelBlock ? kCirBlock : kLevelBlock
 #ifndef ARV_GBM_QUAD  // four-uniform passes in the Gaussian level kernels (see as241_f64_batch)
 #define ARV_GBM_QUAD 1
 #endif
+#ifndef ARV_GBM_SMEM_ROWS  // AS241 coefficient rows from shared memory instead of L1 (__ldg)
+#define ARV_GBM_SMEM_ROWS 1
+#endif
 #ifndef ARV_GBM_MINB_PCG  // GBM + PCG32 instances fit 64 registers without spills (1.3% faster)
 #define ARV_GBM_MINB_PCG 4
 #endif
@@ -278,8 +281,11 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
                                                                 int64_t K1, double *__restrict__ parts,
                                                                 double *__restrict__ paths) {
     extern __shared__ double smd[];
+    __shared__ double2 as241_rows[ARV_GBM_SMEM_ROWS ? 16 : 1];
     for (int i = threadIdx.x; i < (DEG + 1) * K1; i += blockDim.x) smd[i] = __ldg(coeffs + i);
+    if (ARV_GBM_SMEM_ROWS) as241_stage_rows(as241_rows);
     __syncthreads();
+    const double2 *rows = ARV_GBM_SMEM_ROWS ? as241_rows : nullptr;
     constexpr bool GBM = SCHEME == ARV_SCHEME_EM || SCHEME == ARV_SCHEME_MILSTEIN;
     constexpr bool MIL = SCHEME == ARV_SCHEME_MILSTEIN || SCHEME == ARV_SCHEME_CIR_MILSTEIN_TRUNCATED;
 
@@ -310,7 +316,7 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
             bool lo[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) u[k] = rng.next(lo[k]);
-            as241_f64_batch<4, true>(u, z);
+            as241_f64_batch<4, true>(u, z, rows);
 #pragma unroll
             for (int k = 0; k < 4; ++k) w[k] = gauss_table_eval<DEG>(smd, K1, u[k], lo[k]);
             pair_step(z, w);
@@ -322,7 +328,7 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
             bool lo[2];
             u[0] = rng.next(lo[0]);
             u[1] = rng.next(lo[1]);
-            as241_f64_batch<2, true>(u, z);
+            as241_f64_batch<2, true>(u, z, rows);
             w[0] = gauss_table_eval<DEG>(smd, K1, u[0], lo[0]);
             w[1] = gauss_table_eval<DEG>(smd, K1, u[1], lo[1]);
             pair_step(z, w);
