@@ -251,8 +251,13 @@ def run_level(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, *, path_lo: in
     ns = _native_spec(spec, stream, n_paths, path_lo, count)
     stats = torch.empty(NSLOT * 3, dtype=torch.float64, device=device)
     paths = torch.empty((4, count), dtype=torch.float64, device=device) if want_paths else None
-    ws_fn = nat.lib.arv_mlmc_cir_workspace_bytes if spec.scheme == "cir_exact" else nat.lib.arv_mlmc_workspace_bytes
-    ws_bytes = int(ws_fn(count))
+    ws_bytes = int(nat.lib.arv_mlmc_workspace_bytes(count))
+    if spec.scheme == "cir_exact":
+        # segmented CIR levels (records re-bucketed by lambda between segments,
+        # ~84 B per path) when that fits comfortably; else the one-kernel form
+        seg_bytes = int(nat.lib.arv_mlmc_cir_workspace_bytes(count))
+        if seg_bytes <= torch.cuda.mem_get_info(device)[0] // 4:
+            ws_bytes = seg_bytes
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
     s = dev.stream_handle(device)
     pp = paths.data_ptr() if paths is not None else None
