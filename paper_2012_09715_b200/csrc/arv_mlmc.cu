@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kCirBlock, ARV_CIR_MINB) k_cir_exact_level(Lev
             x_a = __dmul_rn(A.scale, ncchi2_eval1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_a));
             // mlmc.py:269-278 exact side, warm-started from the table
             lam_e = __dmul_rn(x_e, A.decay_over_scale);
-            warm = ncchi2_eval1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_e);
+            warm = ncchi2_warm1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_e);
         }
         if constexpr (SORT) {
             const int t = threadIdx.x;
