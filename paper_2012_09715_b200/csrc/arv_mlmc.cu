@@ -213,7 +213,7 @@ __device__ __forceinline__ void cta_moments(const double (&d)[NK], bool valid, d
 // is non-negative), each a fixed-order block reduction (thread t takes
 // partials t, t + B, ...; xor-shuffle tree; warps summed in order), so the
 // result is bitwise reproducible.
-template <int NK>
+template <int NK, int BS = kFinalBlock>
 __device__ __forceinline__ void block_sum(double (&v)[NK], double (*sh)[NK], double *res) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -225,7 +225,7 @@ __device__ __forceinline__ void block_sum(double (&v)[NK], double (*sh)[NK], dou
     __syncthreads();
     if (threadIdx.x < NK) {
         double t = 0.0;
-        for (int w = 0; w < kFinalBlock / 32; ++w) t += sh[w][threadIdx.x];
+        for (int w = 0; w < BS / 32; ++w) t += sh[w][threadIdx.x];
         res[threadIdx.x] = t;
     }
     __syncthreads();
@@ -270,6 +270,80 @@ __global__ void __launch_bounds__(kFinalBlock) k_finalize(const double *__restri
         out[3 * k + 1] = mean[k];
         out[3 * k + 2] = m2[k];
     }
+}
+
+// The same merge over many partials (large levels) in two passes of
+// kFinChunks CTAs: each CTA reduces a fixed contiguous chunk in fixed order,
+// the last CTA to finish (atomic ticket) sums the chunk results in chunk order
+// -- bitwise reproducible, and ~6x faster than one CTA streaming 2 MB twice.
+// PASS 0 yields the count and mean, PASS 1 the M2 about that mean.
+constexpr int kFinStageBlock = 256;
+constexpr int kFinChunks = 64;
+constexpr int64_t kFinSingleMax = 2048;  // up to this many partials: k_finalize
+struct FinScratch {
+    double stage[kFinChunks][2][ARV_NKIND];
+    double cnt_mean[2][ARV_NKIND];
+    unsigned ticket;
+};
+
+template <int NK, int PASS>
+__global__ void __launch_bounds__(kFinStageBlock) k_finalize_chunks(const double *__restrict__ parts,
+                                                                    int64_t n_parts, FinScratch *fs,
+                                                                    double *__restrict__ out) {
+    __shared__ double sh[kFinStageBlock / 32][NK];
+    __shared__ double r0[NK], r1[NK];
+    __shared__ bool last;
+    const int64_t per = (n_parts + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = static_cast<int64_t>(blockIdx.x) * per;
+    const int64_t hi = lo + per < n_parts ? lo + per : n_parts;
+    double a[NK], b[NK], mean[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+        a[k] = b[k] = 0.0;
+        mean[k] = PASS ? __ldcg(&fs->cnt_mean[1][k]) : 0.0;
+    }
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kFinStageBlock) {
+        const double *p = parts + i * NK * 3;
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+            if (PASS == 0) {
+                a[k] += p[3 * k];
+                b[k] = fma(p[3 * k], p[3 * k + 1], b[k]);
+            } else {
+                const double d = p[3 * k + 1] - mean[k];
+                a[k] = fma(p[3 * k] * d, d, a[k] + p[3 * k + 2]);
+            }
+        }
+    }
+    block_sum<NK, kFinStageBlock>(a, sh, r0);
+    if (PASS == 0) block_sum<NK, kFinStageBlock>(b, sh, r1);
+    if (threadIdx.x < NK) {
+        fs->stage[blockIdx.x][0][threadIdx.x] = r0[threadIdx.x];
+        if (PASS == 0) fs->stage[blockIdx.x][1][threadIdx.x] = r1[threadIdx.x];
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&fs->ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x < NK) {
+        const int k = threadIdx.x;
+        double s0 = 0.0, s1 = 0.0;
+        for (unsigned g = 0; g < gridDim.x; ++g) {
+            s0 += __ldcg(&fs->stage[g][0][k]);
+            if (PASS == 0) s1 += __ldcg(&fs->stage[g][1][k]);
+        }
+        if (PASS == 0) {
+            fs->cnt_mean[0][k] = s0;
+            fs->cnt_mean[1][k] = s0 > 0.0 ? s1 / s0 : 0.0;
+        } else {
+            out[3 * k + 0] = __ldcg(&fs->cnt_mean[0][k]);
+            out[3 * k + 1] = __ldcg(&fs->cnt_mean[1][k]);
+            out[3 * k + 2] = s0;
+        }
+    }
+    if (threadIdx.x == 0) fs->ticket = 0u;  // ready for the next pass
 }
 
 // --------------------------------------------------- Gaussian schemes --
@@ -710,8 +784,17 @@ static int fill_common(const arv_level_spec *sp, LevelArgs &A) {
 
 static int64_t n_blocks_for(int64_t count, int bs = kLevelBlock) { return (count + bs - 1) / bs; }
 
-static int run_finalize(double *parts, int64_t nb, double *stats, cudaStream_t s, const char *what) {
-    k_finalize<ARV_NKIND><<<1, kFinalBlock, 0, s>>>(parts, nb, stats);
+static int run_finalize(double *parts, int64_t nb, double *stats, cudaStream_t s, const char *what,
+                        FinScratch *fs = nullptr) {
+    if (!fs || nb <= kFinSingleMax) {
+        k_finalize<ARV_NKIND><<<1, kFinalBlock, 0, s>>>(parts, nb, stats);
+        note_launch();
+        return check_launch(what);
+    }
+    cudaMemsetAsync(&fs->ticket, 0, sizeof(unsigned), s);
+    k_finalize_chunks<ARV_NKIND, 0><<<kFinChunks, kFinStageBlock, 0, s>>>(parts, nb, fs, stats);
+    k_finalize_chunks<ARV_NKIND, 1><<<kFinChunks, kFinStageBlock, 0, s>>>(parts, nb, fs, stats);
+    note_launch();
     note_launch();
     return check_launch(what);
 }
@@ -722,6 +805,14 @@ int g_cir_segment = 4;
 
 static int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
 
+// Chunked-finalize scratch after nb CTA partials in a caller workspace, or
+// nullptr when the workspace holds only the partials (older callers).
+static FinScratch *fin_scratch(void *ws, int64_t ws_bytes, int64_t nb) {
+    const int64_t off = align256(nb * 3 * ARV_NKIND * int64_t(sizeof(double)));
+    return ws_bytes >= off + int64_t(sizeof(FinScratch)) ? reinterpret_cast<FinScratch *>(static_cast<char *>(ws) + off)
+                                                          : nullptr;
+}
+
 // Workspace of a segmented CIR exact level: CTA partials, two record
 // buffers (slot-indexed SoA), buckets, bucket counts / cursors, payoffs.
 struct CirWs {
@@ -729,6 +820,7 @@ struct CirWs {
     double *parts = nullptr, *xe[2] = {}, *xa[2] = {}, *pay = nullptr;
     uint64_t *rs[2] = {};
     uint32_t *fl[2] = {}, *pid[2] = {}, *bucket = nullptr, *hist = nullptr, *cursor = nullptr;
+    FinScratch *fin = nullptr;
     CirWs(int64_t n, void *base) {
         char *p = static_cast<char *>(base);
         auto take = [&](int64_t bytes) -> void * {
@@ -748,6 +840,7 @@ struct CirWs {
         hist = static_cast<uint32_t *>(take(4 * kCirBuckets));
         cursor = static_cast<uint32_t *>(take(4 * kCirBuckets));
         pay = static_cast<double *>(take(16 * n));
+        fin = static_cast<FinScratch *>(take(sizeof(FinScratch)));
     }
 };
 
@@ -759,7 +852,7 @@ extern "C" {
 
 int64_t arv_mlmc_workspace_bytes(int64_t path_count) {
     const int64_t nb = n_blocks_for(path_count < 1 ? 1 : path_count, kMinLevelBlock);
-    return nb * 3 * ARV_NKIND * static_cast<int64_t>(sizeof(double));
+    return align256(nb * 3 * ARV_NKIND * static_cast<int64_t>(sizeof(double))) + int64_t(sizeof(FinScratch));
 }
 
 int64_t arv_mlmc_cir_workspace_bytes(int64_t path_count) {
@@ -816,7 +909,8 @@ int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, in
 #undef ARV_LAUNCH
     note_launch();
     if (int rc = check_launch("arv_mlmc_gaussian_level")) return rc;
-    return run_finalize(parts, nb, stats, s, "arv_mlmc_gaussian_level(finalize)");
+    return run_finalize(parts, nb, stats, s, "arv_mlmc_gaussian_level(finalize)",
+                        fin_scratch(workspace, workspace_bytes, nb));
 }
 
 int arv_mlmc_cir_exact_level(const arv_level_spec *spec, const double *stacks, int64_t n_knots, int degree, int64_t K1,
@@ -881,7 +975,8 @@ int arv_mlmc_cir_exact_level(const arv_level_spec *spec, const double *stacks, i
         G.first = G.last = 1;
         launch(G);
         if (int rc = check_launch("arv_mlmc_cir_exact_level")) return rc;
-        return run_finalize(parts, nb, stats, s, "arv_mlmc_cir_exact_level(finalize)");
+        return run_finalize(parts, nb, stats, s, "arv_mlmc_cir_exact_level(finalize)",
+                            fin_scratch(workspace, workspace_bytes, nb));
     }
     cudaMemsetAsync(W.hist, 0, 4 * kCirBuckets, s);
     for (int64_t k0 = 0; k0 < A.n_f; k0 += seg) {
@@ -916,7 +1011,7 @@ int arv_mlmc_cir_exact_level(const arv_level_spec *spec, const double *stacks, i
     k_cir_payoff_moments<<<(unsigned)nb, kCirBlock, 0, s>>>(A, W.pay, parts, paths);
     note_launch();
     if (int rc = check_launch("arv_mlmc_cir_exact_level(moments)")) return rc;
-    return run_finalize(parts, nb, stats, s, "arv_mlmc_cir_exact_level(finalize)");
+    return run_finalize(parts, nb, stats, s, "arv_mlmc_cir_exact_level(finalize)", W.fin);
 }
 
 int arv_ncchi2_inv_cdf_tol(const double *u, const double *lam, int64_t nlam, double nu, const double *x0, double tol,

@@ -254,9 +254,11 @@ def run_level(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, *, path_lo: in
     ws_bytes = int(nat.lib.arv_mlmc_workspace_bytes(count))
     if spec.scheme == "cir_exact":
         # segmented CIR levels (records re-bucketed by lambda between segments,
-        # ~84 B per path) when that fits comfortably; else the one-kernel form
+        # ~84 B per path) up to an eighth of the device memory; else the
+        # one-kernel form
+        # (device properties are cached; cudaMemGetInfo costs ~0.1 ms per call)
         seg_bytes = int(nat.lib.arv_mlmc_cir_workspace_bytes(count))
-        if seg_bytes <= torch.cuda.mem_get_info(device)[0] // 4:
+        if seg_bytes <= torch.cuda.get_device_properties(device).total_memory // 8:
             ws_bytes = seg_bytes
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
     s = dev.stream_handle(device)

@@ -107,7 +107,8 @@ class TestValidationBeforeCuda:
         s.scheme = nat.SCHEME_EM
         with pytest.raises(errors.ConfigError, match="workspace"):
             nat.call("arv_mlmc_gaussian_level", ctypes.byref(s), None, 1, 16, None, None, None, 0, None)
-        assert nat.lib.arv_mlmc_workspace_bytes(1 << 22) == (1 << 22) // 256 * 15 * 8
+        parts = (1 << 22) // 256 * 15 * 8
+        assert nat.lib.arv_mlmc_workspace_bytes(1 << 22) >= parts  # + chunked-finalize scratch
 
 
 class TestHostMirror:

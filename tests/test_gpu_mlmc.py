@@ -337,3 +337,23 @@ def test_cir_exact_segmented_equals_one_kernel(arv, philox):
         assert torch.equal(bits_t(p), bits_t(p0)), seg
         assert torch.equal(bits_t(st), bits_t(st0)), seg
         assert f == f0
+
+
+@pytest.mark.gpu
+def test_level_statistics_match_path_moments(arv):
+    """The chunked two-pass finalize (> 2048 CTA partials) reproduces the moments
+    of the per-path differences computed on the host from the returned paths."""
+    from paper_2012_09715_b200.mlmc import run_level
+
+    lin = arv.load_table("dyadic_linear_k15")
+    spec = arv.LevelSpec(level=2, scheme="euler_maruyama", process=arv.GbmParams(0.05, 0.2, 1.0, 1.0),
+                         rv_source=lin, kind="four_way", n0=1)
+    n = (1 << 20) + 77  # 4097 CTA partials, ragged last CTA
+    st, paths, _ = run_level(spec, arv.level_stream(3, 2), n, want_paths=True)
+    st = st.cpu().numpy()
+    fe, ce, fa, ca = (p.astype(np.float64) for p in paths.cpu().numpy())
+    kinds = [fe - ce, fa - ca, (fe - ce) - (fa - ca), fe, fa]
+    for k, d in enumerate(kinds):
+        assert st[k, 0] == n
+        np.testing.assert_allclose(st[k, 1], d.mean(), rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(st[k, 2], ((d - d.mean()) ** 2).sum(), rtol=1e-9, atol=1e-18)
