@@ -189,13 +189,26 @@ struct EvalGauss32 {
     }
 };
 // floor(2^q u) for u = (k + 1/2) 2^-23, k = w >> 9: k >> (23-q) for q <= 23,
-// 2k + 1 for q = 24.  Table in shared memory (q <= 14) or global (L2).
-struct EvalConstant {
-    const float *tab;
-    int shift;  // 32 - q, or -1 for q == 24
+// 2k + 1 for q = 24.  Table in shared memory (q <= 14, addressed as a 32-bit
+// shared-space address so the lookup is one LDS -- a generic pointer made it a
+// generic LD with 64-bit address arithmetic) or global (L2).
+struct EvalConstantSmem {
+    uint32_t base;  // shared-space byte address of the table
+    int shift;      // 32 - q
+    uint32_t four;  // 4 in a register: the address is one IMAD
     __device__ __forceinline__ uint32_t operator()(uint32_t w) const {
-        const uint32_t idx = shift >= 0 ? (w >> shift) : (((w >> 9) << 1) | 1u);
-        return __float_as_uint(tab[idx]);
+        return __float_as_uint(lds_f32<0>(mad_u32(w >> shift, four, base)));
+    }
+};
+struct EvalConstantGlobal {
+    const float *tab;
+    int shift;  // 32 - q
+    __device__ __forceinline__ uint32_t operator()(uint32_t w) const { return __float_as_uint(__ldg(tab + (w >> shift))); }
+};
+struct EvalConstant24 {
+    const float *tab;
+    __device__ __forceinline__ uint32_t operator()(uint32_t w) const {
+        return __float_as_uint(__ldg(tab + ((((w >> 9) << 1) | 1u))));
     }
 };
 
@@ -294,19 +307,23 @@ __global__ void __launch_bounds__(256, ARV_GEN_MINB) k_gen_simple(GenArgs a, uin
     gen_dispatch<MODE>(a, out, eval);
 }
 
-template <int MODE>
+// KIND: 0 = table in shared memory (q <= 14), 1 = global (q <= 23), 2 = global, q = 24.
+template <int MODE, int KIND>
 __global__ void __launch_bounds__(256, ARV_GEN_MINB) k_pcg32_constant(GenArgs a, const float *__restrict__ values, int q,
-                                                        int use_smem, uint32_t *out) {
-    extern __shared__ float4 smem4[];
-    float *sm = reinterpret_cast<float *>(smem4);
-    const float *tab = values;
-    if (use_smem) {
+                                                        uint32_t *out) {
+    if constexpr (KIND == 0) {
+        extern __shared__ float4 smem4[];
+        float *sm = reinterpret_cast<float *>(smem4);
         const int nv = 1 << q;
         for (int i = threadIdx.x; i < nv; i += blockDim.x) sm[i] = __ldg(values + i);
         __syncthreads();
-        tab = sm;
+        const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+        gen_dispatch<MODE>(a, out, EvalConstantSmem{base, 32 - q, 4u + threadIdx.x * a.zero32});
+    } else if constexpr (KIND == 1) {
+        gen_dispatch<MODE>(a, out, EvalConstantGlobal{values, 32 - q});
+    } else {
+        gen_dispatch<MODE>(a, out, EvalConstant24{values});
     }
-    gen_dispatch<MODE>(a, out, EvalConstant{tab, q <= 23 ? 32 - q : -1});
 }
 
 template <int DEG, int MODE>
@@ -473,24 +490,20 @@ int arv_pcg32_constant_f32(uint64_t seed, uint64_t stream_id, uint64_t offset, c
     if (q < 1 || q > 24) return set_error(ARV_ERR_CONFIG, "interval exponent q must be in [1, 24], got %d", q);
     if (n < 0) return set_error(ARV_ERR_CONFIG, "negative n");
     if (n == 0) return ARV_OK;
-    const int use_smem = q <= 14;
-    const size_t smem = use_smem ? (sizeof(float) << q) : 0;
+    const int kind = q <= 14 ? 0 : (q <= 23 ? 1 : 2);
+    const size_t smem = kind == 0 ? (sizeof(float) << q) : 0;
     const int mode = store_mode(out);
-    const void *fn = mode == 8   ? (const void *)k_pcg32_constant<8>
-                     : mode == 4 ? (const void *)k_pcg32_constant<4>
-                                 : (const void *)k_pcg32_constant<1>;
+#define ARV_CONST_FN(M) \
+    (kind == 0 ? (const void *)k_pcg32_constant<M, 0> : kind == 1 ? (const void *)k_pcg32_constant<M, 1> : (const void *)k_pcg32_constant<M, 2>)
+    const void *fn = mode == 8 ? ARV_CONST_FN(8) : mode == 4 ? ARV_CONST_FN(4) : ARV_CONST_FN(1);
+#undef ARV_CONST_FN
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = gen_grid(fn, n, mode, smem);
     const int64_t T = static_cast<int64_t>(grid) * kGenBlock;
     const GenArgs a = make_gen_args(seed, stream_id, offset, n, T, mode == 1 ? 4 : mode);
     uint32_t *o = reinterpret_cast<uint32_t *>(out);
-    cudaStream_t s = as_stream(stream);
-#define ARV_CONST(M)                                                                                        \
-    k_pcg32_constant<M><<<grid, kGenBlock, smem, s>>>(a, values, q, use_smem, o)
-    if (mode == 8) ARV_CONST(8);
-    else if (mode == 4) ARV_CONST(4);
-    else ARV_CONST(1);
-#undef ARV_CONST
+    void *args[] = {(void *)&a, (void *)&values, (void *)&q, (void *)&o};
+    cudaLaunchKernel(fn, dim3(grid), dim3(kGenBlock), args, smem, as_stream(stream));
     note_launch();
     return check_launch("arv_pcg32_constant_f32");
 }
