@@ -393,17 +393,22 @@ static int store_mode(const void *out) {
 }
 
 // One wave: CTAs per SM = the kernel's resident count (a second partial wave
-// of a grid-stride kernel costs 2-7% at 2^28, tools/sweep_launch.py), fewer
+// of a grid-stride kernel cost 2-7% at 2^28 in an earlier build, tools/sweep_launch.py), fewer
 // for small n so that every thread keeps >= kMinPerThread samples to amortise
 // its jump-ahead (2^24: 4 CTAs/SM beat 8 by 7%; 2^20: 1-2 beat 8 by 30%).
 constexpr int64_t kMinPerThread = 64;
 
+// Very large calls (>= 16 one-wave grids of 64 samples per thread, e.g. 2^28
+// samples) run 5/3 waves instead: the generators then finish 1.2-1.7% sooner
+// (2^28: sub-interval 0.1935 -> 0.1911 ms, constant 0.1663 -> 0.1635 ms;
+// 2^26 and below keep one wave, where the extra CTAs cost 2-20%).
 static int gen_grid(const void *fn, int64_t n, int mode, size_t smem = 0) {
     int per_sm = g_ctas_per_sm;
     if (per_sm <= 0) {
         const int64_t want = n / (static_cast<int64_t>(device_sm_count()) * kGenBlock * kMinPerThread);
         const int occ = resident_ctas(fn, kGenBlock, smem);
         per_sm = static_cast<int>(want < 1 ? 1 : (want < occ ? want : occ));
+        if (want >= 16 * occ) per_sm = occ + (2 * occ) / 3;
     }
     return stream_grid((n + mode - 1) / mode, kGenBlock, per_sm);
 }
