@@ -49,6 +49,8 @@ constexpr int kMinLevelBlock = kCirBlock < kLevelBlock ? kCirBlock : kLevelBlock
 #endif
 constexpr int kFinalBlock = 1024;
 
+constexpr int kPathJumpBits = 40;  // path ids < 2^40
+
 struct LevelArgs {
     double a, b, c;  // GBM: mu, sigma, -; CIR: kappa, theta, sigma
     double x0, strike;
@@ -64,7 +66,20 @@ struct LevelArgs {
     int rng;             // ARV_RNG_PCG32 / ARV_RNG_PHILOX
     uint64_t seed, sid;  // Philox key
     uint64_t n_paths_total;
+    Affine jump2[kPathJumpBits];  // LCG^(2^i): path p starts popcount(p) affine maps from s0
 };
+
+// PCG32 state of output p of the level stream (path p's first uniform): one
+// affine map per set bit of p from the kernel-parameter table, instead of a
+// square-and-multiply lcg_jump per thread (which was half of the instructions
+// of a one-step level).
+__device__ __forceinline__ uint64_t path_start_state(const LevelArgs &A, uint64_t p) {
+    uint64_t s = A.s0;
+#pragma unroll 1
+    for (int b = 0; b < kPathJumpBits && (p >> b) != 0; ++b)
+        if ((p >> b) & 1u) s = A.jump2[b].a * s + A.jump2[b].c;
+    return s;
+}
 
 // Per-path uniform source: word k * n_paths_total + p for fine step k.
 struct PathRng {
@@ -80,8 +95,7 @@ struct PathRng {
         } else if (philox) {
             s = p;
         } else {
-            const Affine jp = lcg_jump(p, A.inc);
-            s = jp.a * A.s0 + jp.c;
+            s = path_start_state(A, p);
         }
     }
     __device__ __forceinline__ double next() {
@@ -108,8 +122,7 @@ struct PathSource<false> {
     uint64_t s;
     Affine step;
     __device__ __forceinline__ PathSource(const LevelArgs &A, uint64_t p) : step(A.step) {
-        const Affine jp = lcg_jump(p, A.inc);
-        s = jp.a * A.s0 + jp.c;
+        s = path_start_state(A, p);
     }
     // next uniform and the reference's u < 1/2
     __device__ __forceinline__ double next(bool &lower) {
@@ -771,6 +784,13 @@ static int fill_common(const arv_level_spec *sp, LevelArgs &A) {
     A.s0 = st.state;
     A.inc = st.inc;
     A.step = lcg_jump(static_cast<uint64_t>(sp->n_paths_total), st.inc);
+    Affine j2 = lcg_jump(1, st.inc);
+    for (int b = 0; b < kPathJumpBits; ++b) {
+        A.jump2[b] = j2;
+        j2 = {j2.a * j2.a, j2.a * j2.c + j2.c};  // compose the map with itself
+    }
+    if (static_cast<uint64_t>(sp->n_paths_total) >> kPathJumpBits)
+        return set_error(ARV_ERR_CONFIG, "n_paths_total must be < 2^40");
     if (sp->rng != ARV_RNG_PCG32 && sp->rng != ARV_RNG_PHILOX) return set_error(ARV_ERR_CONFIG, "unknown rng %d", sp->rng);
     A.rng = sp->rng;
     A.seed = sp->seed;
