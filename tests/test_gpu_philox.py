@@ -76,3 +76,13 @@ def test_gbm_replays_reference_paths(arv, golden, hashes):
         for row, key in enumerate(("two_way_exact", "two_way_approx", "four_way")):
             np.testing.assert_allclose(suite[key].mean, rs[row, 0], rtol=1e-11, atol=1e-16)
             np.testing.assert_allclose(suite[key].variance, rs[row, 1], rtol=1e-9, atol=1e-20)
+
+
+def test_aligned_vector_path(arv, orc):
+    """4-word-aligned counters take the 16-byte-store path; ragged tails and
+    mid-block starts the scalar one -- both bit-exact with the oracle."""
+    for counter, n in ((0, (1 << 16) + 3), (4, 4097), (8, 1), (12, 6)):
+        u = arv.PhiloxStream(9, 4, counter=counter).uniforms(n)
+        assert np.array_equal(bits(u), bits(orc.philox_uniforms(9, 4, counter, n))), (counter, n)
+        w = arv.PhiloxStream(9, 4, counter=counter).raw_words(n).cpu().numpy()
+        assert np.array_equal(w, orc.philox_words(9, 4, counter, n)), (counter, n)
