@@ -172,6 +172,17 @@ __device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, do
     }
     double G = exp(lg);
     double P = G;                    // P(a0 + j) ~ G(a0 + j)
+#if ARV_NC_BLOCK
+    if (L.blocked && j - top <= ARV_NC_BLOCK) {  // bulk: incremental factor (see the window loop)
+        double f = fma(jd, inv_y, a0y);
+        jd -= static_cast<double>(j > top ? j - top : 0);
+        for (; j > top; --j) {
+            G *= f;
+            P += G;
+            f -= inv_y;
+        }
+    }
+#endif
     for (; j > top; --j) {           // above the Poisson window: P and G only
         G *= fma(jd, inv_y, a0y);    // G(a0 + j - 1) = G(a0 + j) (a0 + j) / y
         P += G;
