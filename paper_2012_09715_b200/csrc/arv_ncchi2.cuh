@@ -132,7 +132,8 @@ __device__ inline NcLam nc_lam(double lam, double sigmas = kNcSigmas) {
     L.h = 0.5 * lam;
     L.sigmas = sigmas;
     const int k = static_cast<int>(floor(L.h));
-    const int wp = L.h < 1e-2 ? 8 : static_cast<int>(sigmas * sqrt(L.h)) + 10;
+    // window extents are integer heuristics: f32 square roots suffice
+    const int wp = L.h < 1e-2 ? 8 : static_cast<int>(static_cast<float>(sigmas) * sqrtf(static_cast<float>(L.h))) + 10;
     L.top = k + wp;
     L.bot = k - wp > 0 ? k - wp : 0;
     L.inv_h = L.h > 0.0 ? 1.0 / L.h : 0.0;
@@ -156,7 +157,7 @@ template <bool FULL>
 __device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, double u, double &inv_w) {
     const double y = 0.5 * x;
     const int top = L.top, bot = L.bot;
-    const int jy = static_cast<int>(ceil(y - a0)) + static_cast<int>(L.sigmas * sqrt(y)) + 10;
+    const int jy = static_cast<int>(ceil(y - a0)) + static_cast<int>(static_cast<float>(L.sigmas) * sqrtf(static_cast<float>(y))) + 10;
     int j = jy > top ? jy : top;
     const double inv_y = 1.0 / y;
     const double a0y = a0 * inv_y;
@@ -340,7 +341,7 @@ __device__ unsigned long long g_nc_evals, g_nc_solves, g_nc_hist[8], g_nc_warp_h
 __device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, double x0, double tol = 1e-9) {
     const double a0 = 0.5 * nu;
     const double one_minus_u = 1.0 - u;
-    double hi = lam + nu + 20.0 * sqrt(2.0 * (lam + nu)) + 100.0;
+    double hi = lam + nu + 20.0 * static_cast<double>(sqrtf(static_cast<float>(2.0 * (lam + nu)))) + 100.0;  // bracket heuristic
     double lo = 0.0;
     const double tol_f = fmin(tol, fmax(1e-13, 1e-4 * fmin(u, one_minus_u)));
     double x = x0 > 0.0 ? x0 : lam + nu;
