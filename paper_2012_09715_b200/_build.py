@@ -24,6 +24,12 @@ LIB_NAME = "libarv_b200.so"
 LIB_PATH = os.path.join(PKG_DIR, LIB_NAME)
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# The MLMC level kernels instantiate the same ncchi2 quantile code in several
+# kernels (with / without the CTA sort, one-kernel / segmented); with implicit
+# mul+add contraction ptxas may fuse differently per instantiation, so per-path
+# results would depend on the launch form.  Every intended FMA there is
+# written explicitly (fma()), so contraction is switched off for that file.
+PER_FILE_FLAGS = {"arv_mlmc.cu": ["-fmad=false"]}
 
 
 def nvcc_path() -> str:
@@ -68,7 +74,7 @@ def build(verbose_ptxas: bool = False, force: bool = False, defines=(), out: str
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
-        procs.append(subprocess.Popen([nvcc, *common, "-c", src, "-o", obj]))
+        procs.append(subprocess.Popen([nvcc, *common, *PER_FILE_FLAGS.get(os.path.basename(src), []), "-c", src, "-o", obj]))
     bad = [p.args[-3] for p in procs if p.wait() != 0]
     if bad:
         raise RuntimeError(f"nvcc failed for {bad}")

@@ -108,8 +108,18 @@ struct NcCdf {
 #ifndef ARV_NC_SIGMAS_BULK
 #define ARV_NC_SIGMAS_BULK 7.0
 #endif
+#ifndef ARV_NC_NARROW_START
+#define ARV_NC_NARROW_START 1
+#endif
+#ifndef ARV_NC_SIGMAS_START
+#define ARV_NC_SIGMAS_START 6.0
+#endif
 constexpr double kNcSigmas = ARV_NC_SIGMAS;
 constexpr double kNcSigmasBulk = ARV_NC_SIGMAS_BULK;
+// First sweep of a bulk solve: it only places the Taylor step, whose result
+// the full-width verification sweep then checks against tol_f >= 1e-10, so a
+// 6-sigma window (truncation ~1e-11..1e-10) suffices there.
+constexpr double kNcSigmasStart = ARV_NC_SIGMAS_START;
 
 #ifndef ARV_NC_BLOCK
 #define ARV_NC_BLOCK 128  // terms per block of incremental factors (0: exact factors every term)
@@ -125,6 +135,7 @@ struct NcLam {
     double h, inv_h, p_top, sigmas;
     int top, bot;
     bool blocked;  // bulk quantile solve: incremental sweep factors allowed
+    int top_n, bot_n;  // narrower window for a bulk solve's first (Taylor-start) sweep
 };
 
 __device__ inline NcLam nc_lam(double lam, double sigmas = kNcSigmas) {
@@ -139,6 +150,9 @@ __device__ inline NcLam nc_lam(double lam, double sigmas = kNcSigmas) {
     L.inv_h = L.h > 0.0 ? 1.0 / L.h : 0.0;
     L.p_top = L.h > 0.0 ? exp(nc_logdens(static_cast<double>(L.top), L.h)) : 0.0;
     L.blocked = sigmas < kNcSigmas && (L.top - L.bot + 1) <= ARV_NC_BLOCK_MAXW;
+    const int wn = L.h < 1e-2 ? 8 : static_cast<int>(static_cast<float>(kNcSigmasStart) * sqrtf(static_cast<float>(L.h))) + 10;
+    L.top_n = k + wn < L.top ? k + wn : L.top;
+    L.bot_n = k - wn > L.bot ? k - wn : L.bot;
     return L;
 }
 
@@ -153,11 +167,12 @@ __device__ inline NcLam nc_lam(double lam, double sigmas = kNcSigmas) {
 #ifndef ARV_NC_NORMALISE
 #define ARV_NC_NORMALISE 0
 #endif
-template <bool FULL>
+template <bool FULL, bool NARROW = false>
 __device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, double u, double &inv_w) {
     const double y = 0.5 * x;
-    const int top = L.top, bot = L.bot;
-    const int jy = static_cast<int>(ceil(y - a0)) + static_cast<int>(static_cast<float>(L.sigmas) * sqrtf(static_cast<float>(y))) + 10;
+    const int top = NARROW ? L.top_n : L.top, bot = NARROW ? L.bot_n : L.bot;
+    const float sig = NARROW ? static_cast<float>(kNcSigmasStart) : static_cast<float>(L.sigmas);
+    const int jy = static_cast<int>(ceil(y - a0)) + static_cast<int>(sig * sqrtf(static_cast<float>(y))) + 10;
     int j = jy > top ? jy : top;
     const double inv_y = 1.0 / y;
     const double a0y = a0 * inv_y;
@@ -192,6 +207,9 @@ __device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, do
     if (L.h > 0.0) {
         const double inv_h = L.inv_h;
         double p = L.p_top;
+        if constexpr (NARROW) {  // Poisson weight at the narrow window top
+            for (int i = L.top; i > top; --i) p *= static_cast<double>(i) * inv_h;
+        }
         double wsum = 0.0, acc = 0.0, dens = 0.0, s0 = 0.0;
         for (int i = top; i > j && i >= bot; --i) {  // window indices whose gamma terms underflowed
             if constexpr (FULL && ARV_NC_NORMALISE) wsum += p;
@@ -348,7 +366,10 @@ __device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, do
     x = fmin(fmax(x, 1e-8), hi);
     const NcLam L = nc_lam(lam, fmin(u, one_minus_u) >= 1e-6 ? kNcSigmasBulk : kNcSigmas);
     double inv_w;
-    NcCdf c = ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w);
+    // bulk solves: the first sweep only places the Taylor step (6-sigma window);
+    // the verification and any further sweeps use the full window
+    NcCdf c = L.blocked && ARV_NC_NARROW_START ? ncchi2_cdf_sweep<true, true>(a0, x, L, u, inv_w)
+                                               : ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w);
 #if ARV_NC_COUNT
     int n_eval = 1;
 #endif
