@@ -159,14 +159,11 @@ __device__ inline NcLam nc_lam(double lam, double sigmas = kNcSigmas) {
 // F(x) - u for x > 0, a0 = nu / 2.  FULL: also the density f(x) = S_1 / 2
 // and S_0 (for the Taylor step).  !FULL (a verification evaluation of the
 // same solve): F only -- 7 instead of 9 FP64 operations per window term.
-// The Poisson weights are not renormalised by their window sum
-// (ARV_NC_NORMALISE=0): p_top is Loader's saddle-point pmf (a few ulp), the
+// The Poisson weights are not renormalised by their window sum: p_top is
+// Loader's saddle-point pmf (a few ulp), the
 // window drops < 1e-15 of the Poisson mass, and the downward recurrence
 // drifts by ~(window length) ulp, so F moves by < 1e-13 and one FP64
 // operation per term is saved.
-#ifndef ARV_NC_NORMALISE
-#define ARV_NC_NORMALISE 0
-#endif
 template <bool FULL, bool NARROW = false>
 __device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, double u, double &inv_w) {
     const double y = 0.5 * x;
@@ -210,16 +207,14 @@ __device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, do
         if constexpr (NARROW) {  // Poisson weight at the narrow window top
             for (int i = L.top; i > top; --i) p *= static_cast<double>(i) * inv_h;
         }
-        double wsum = 0.0, acc = 0.0, dens = 0.0, s0 = 0.0;
+        double acc = 0.0, dens = 0.0, s0 = 0.0;
         for (int i = top; i > j && i >= bot; --i) {  // window indices whose gamma terms underflowed
-            if constexpr (FULL && ARV_NC_NORMALISE) wsum += p;
             p *= static_cast<double>(i) * inv_h;
         }
         auto term = [&](double fj, double rj) {
             acc = fma(p, P, acc);
             const double Gm = G * fj;  // G(a0 + j - 1)
             if constexpr (FULL) {
-                if constexpr (ARV_NC_NORMALISE) wsum += p;
                 s0 = fma(p, G, s0);
                 dens = fma(p, Gm, dens);
             }
@@ -257,7 +252,7 @@ __device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, do
             term(fma(jd, inv_y, a0y), jd * inv_h);
             jd -= 1.0;
         }
-        if constexpr (FULL) inv_w = ARV_NC_NORMALISE ? 1.0 / wsum : 1.0;
+        if constexpr (FULL) inv_w = 1.0;
         return {fma(acc, inv_w, -u), 0.5 * dens * inv_w, s0 * inv_w};
     }
     // h == 0: the central law, F = P(a0, y), f = G(a0 - 1, y) / 2
@@ -279,9 +274,6 @@ struct NcQuantile {
     double resid;  // |F(x) - u|
 };
 
-#ifndef ARV_NC_HALLEY
-#define ARV_NC_HALLEY 1
-#endif
 // Degree of the Taylor-polynomial step (0: Newton / Halley steps instead).
 #ifndef ARV_NC_TAYLOR
 #define ARV_NC_TAYLOR 4
@@ -350,12 +342,11 @@ __device__ unsigned long long g_nc_evals, g_nc_solves, g_nc_hist[8], g_nc_warp_h
 
 // exact_dist.py:381-461 contract, per element, warm start x0 (<= 0: mean);
 // tol is the reference's `tol` argument (default 1e-9).  Same bracket,
-// tolerance and 1e-8 residual contract as _vector_newton; from the second
-// step on the Newton step gets Halley's curvature correction (F'' estimated
-// from the last two density values), which the bracket safeguard accepts or
-// replaces by bisection exactly as for a Newton step.  With the table warm
-// start 98.5% of solves finish in 3 CDF evaluations and 0.1% of warps need a
-// 4th (plain Newton: 3.3% of solves, 66% of warps) -- level 6 48 -> 42.5 ms.
+// tolerance and 1e-8 residual contract as _vector_newton: each step is the
+// Taylor-polynomial root (nc_taylor_step; plain Newton if it is not finite),
+// which the bracket safeguard accepts or replaces by bisection.  From the
+// table warm start 99.99% of solves finish after the start sweep and one
+// verification sweep (tools/nc_diag.py).
 __device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, double x0, double tol = 1e-9) {
     const double a0 = 0.5 * nu;
     const double one_minus_u = 1.0 - u;
@@ -373,9 +364,6 @@ __device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, do
 #if ARV_NC_COUNT
     int n_eval = 1;
 #endif
-#if ARV_NC_HALLEY && !ARV_NC_TAYLOR
-    double x_prev = 0.0, pdf_prev = 0.0;
-#endif
     for (int it = 0; it < 80; ++it) {
         if (fabs(c.resid) <= tol_f) break;
         if (c.resid > 0.0) hi = x;
@@ -385,19 +373,6 @@ __device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, do
         if (!isfinite(dx)) dx = c.resid / c.pdf;  // Newton
 #else
         double dx = c.resid / c.pdf;  // Newton
-#endif
-#if ARV_NC_HALLEY && !ARV_NC_TAYLOR
-        if (it > 0 && x != x_prev) {
-            // Halley with the density slope from the last two iterates (a free
-            // secant estimate of F''): near-cubic second step, so far fewer
-            // lanes need a 4th CDF evaluation -- in a warp the slowest lane
-            // sets the pace (tools/nc_diag.py).  Plain Newton if it misbehaves.
-            const double fp = (c.pdf - pdf_prev) / (x - x_prev);
-            const double den = 1.0 - 0.5 * dx * fp / c.pdf;
-            if (den > 0.5 && den < 2.0) dx /= den;
-        }
-        x_prev = x;
-        pdf_prev = c.pdf;
 #endif
         double xn = x - dx;
         if (!isfinite(xn) || xn <= lo || xn >= hi) xn = 0.5 * (lo + hi);
