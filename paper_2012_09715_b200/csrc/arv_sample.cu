@@ -49,11 +49,25 @@ struct GenArgs {
     Affine pow2[kJumpBits];  // LCG^(G 2^i): a thread reaches group g0 with popcount(g0) steps
 };
 
-// State of the first sample of group g0 (g0 < 2^kJumpBits).
+// State of the first sample of group g0 = blockIdx.x * 256 + threadIdx.x
+// (g0 < 2^kJumpBits, blockDim.x = 256): thread 0 walks the CTA's high bits
+// once and shares the state; each thread then walks only its 8 low bits
+// (powers of one affine map commute).  A full 24-bit walk per thread was ~20%
+// of a thread's work at 2^24 samples.
 __device__ __forceinline__ uint64_t group_start(const GenArgs &a, uint64_t g0) {
-    uint64_t s = a.s_base;
+    __shared__ uint64_t s_cta;
+    if (threadIdx.x == 0) {
+        uint64_t s = a.s_base;
+        const uint64_t hb = g0 >> 8;
 #pragma unroll 1
-    for (int i = 0; i < kJumpBits; ++i)
+        for (int i = 8; i < kJumpBits && (hb >> (i - 8)) != 0; ++i)
+            if ((g0 >> i) & 1u) s = a.pow2[i].a * s + a.pow2[i].c;
+        s_cta = s;
+    }
+    __syncthreads();
+    uint64_t s = s_cta;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
         if ((g0 >> i) & 1u) s = a.pow2[i].a * s + a.pow2[i].c;
     return s;
 }
