@@ -46,6 +46,7 @@ struct GenArgs {
     int64_t n;
     uint64_t zero;    // always 0: makes derived constants per-thread registers
     uint32_t zero32;
+    uint64_t iter_q, iter_r;  // (n / G) = iter_q * T + iter_r: thread g0 runs iter_q + (g0 < iter_r) groups
     Affine pow2[kJumpBits];  // LCG^(G 2^i): a thread reaches group g0 with popcount(g0) steps
 };
 
@@ -82,6 +83,9 @@ static GenArgs make_gen_args(uint64_t seed, uint64_t stream_id, uint64_t offset,
     a.n = n;
     a.zero = 0;
     a.zero32 = 0;
+    const uint64_t n_full = static_cast<uint64_t>(n) / static_cast<uint64_t>(G);
+    a.iter_q = n_full / static_cast<uint64_t>(total_threads);
+    a.iter_r = n_full % static_cast<uint64_t>(total_threads);
     Affine p = lcg_jump(static_cast<uint64_t>(G), st.inc);
     for (int i = 0; i < kJumpBits; ++i) {
         a.pow2[i] = p;
@@ -139,7 +143,8 @@ __device__ __forceinline__ void gen_loop_vec(const GenArgs &a, uint32_t *__restr
     const Affine st{a.stride.a + z, a.stride.c + z};
     const uint32_t m19 = (1u << 19) + static_cast<uint32_t>(z), m5 = 32u + static_cast<uint32_t>(z);
     // Trip count once; the loop runs on a 32-bit counter and a pointer bump.
-    const uint32_t iters = g0 < n_full ? static_cast<uint32_t>((n_full - g0 + T - 1) / T) : 0u;
+    // host-computed quotient / remainder: no 64-bit division per thread
+    const uint32_t iters = static_cast<uint32_t>(a.iter_q) + (g0 < a.iter_r ? 1u : 0u);
     uint32_t *p = out + G * g0;
     const uint64_t step = G * T;
 #pragma unroll kGenUnroll
