@@ -28,6 +28,9 @@ namespace arv {
 #ifndef ARV_GEN_MINB
 #define ARV_GEN_MINB 6
 #endif
+#ifndef ARV_GEN_PDL
+#define ARV_GEN_PDL 1
+#endif
 #ifndef ARV_GEN_UNROLL
 #define ARV_GEN_UNROLL 2
 #endif
@@ -148,6 +151,12 @@ __device__ __forceinline__ void gen_loop_vec(const GenArgs &a, uint32_t *__restr
     uint32_t *p = out + G * g0;
     const uint64_t step = G * T;
 #pragma unroll kGenUnroll
+#if ARV_GEN_PDL
+    // Programmatic dependent launch: the prologue above (table staging, start
+    // state) may overlap the previous kernel's tail on the stream; wait for it
+    // to complete (and its stores to be visible) before storing.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
     for (uint32_t it = 0; it < iters; ++it) {
         uint32_t w[G];
 #pragma unroll
@@ -348,6 +357,10 @@ __global__ void __launch_bounds__(256, ARV_GEN_MINB) k_pcg32_constant(GenArgs a,
 template <int DEG, int MODE>
 __global__ void __launch_bounds__(256, ARV_GEN_MINB) k_pcg32_subdyadic(GenArgs a, const float *__restrict__ coeffs, int K, int b,
                                                          uint32_t *out) {
+#if ARV_GEN_PDL
+    // let the next kernel on the stream start its CTAs as ours retire
+    asm volatile("griddepcontrol.launch_dependents;");
+#endif
     __shared__ float sm[(DEG + 1) * kLatticePlane];
     stage_subdyadic<DEG>(sm, coeffs, K, b);
     const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sm)) - 4u * (kLatticeE0 << b);
@@ -463,6 +476,23 @@ static void launch_subdyadic(uint64_t seed, uint64_t sid, uint64_t offset, const
     const GenArgs a = make_gen_args(seed, sid, offset, n, T, mode == 1 ? 4 : mode);
     uint32_t *o = reinterpret_cast<uint32_t *>(out);
     cudaStream_t s = as_stream(stream);
+#if ARV_GEN_PDL
+    if (mode != 1) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kGenBlock);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (mode == 8) cudaLaunchKernelEx(&cfg, k_pcg32_subdyadic<D, 8>, a, coeffs, K, sub_bits, o);
+        else cudaLaunchKernelEx(&cfg, k_pcg32_subdyadic<D, 4>, a, coeffs, K, sub_bits, o);
+        return;
+    }
+#endif
     if (mode == 8) k_pcg32_subdyadic<D, 8><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o);
     else if (mode == 4) k_pcg32_subdyadic<D, 4><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o);
     else k_pcg32_subdyadic<D, 1><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o);
