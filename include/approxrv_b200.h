@@ -48,6 +48,8 @@ extern "C" {
 /* ---- library ----------------------------------------------------------- */
 ARV_API int arv_abi_version(void);
 ARV_API const char *arv_last_error(void);
+/* sha256 (hex) of the sources the library was built from. */
+ARV_API const char *arv_source_hash(void);
 /* Number of kernel launches this library has issued (process-wide). */
 ARV_API uint64_t arv_launch_count(void);
 
@@ -102,6 +104,15 @@ ARV_API int arv_pcg32_constant_f32(uint64_t seed, uint64_t stream_id, uint64_t o
  * reference K=15 layout is sub_bits = 0 with coeffs[d][j-1][0] = ref[d][j]. */
 ARV_API int arv_pcg32_subdyadic_f32(uint64_t seed, uint64_t stream_id, uint64_t offset, const float *coeffs,
                             int degree, int K, int sub_bits, float *out, int64_t n, void *stream);
+/* Exhaustive check hook (tests): out f32[2^23] receives the fused
+ * generators' evaluator at every point of the f32 lattice, out[k] = eval(w)
+ * for a word w with w >> 9 == k.  mode 0 = the general evaluator
+ * (k_pcg32_subdyadic); mode 1 = the degree-1 signed-table evaluator
+ * (k_pcg32_linsigned, sub_bits <= 4) including its per-table exactness check
+ * and fallback; *fast (device int32[1], may be NULL) receives 1 if the
+ * signed evaluator ran, 0 if the table failed the check. */
+ARV_API int arv_lattice_subdyadic_f32(const float *coeffs, int degree, int K, int sub_bits, int mode, float *out,
+                                      int *fast, void *stream);
 /* exact comparators: AS241 of the same f32-lattice uniforms, f64 / f32 out */
 ARV_API int arv_pcg32_gaussian_f64(uint64_t seed, uint64_t stream_id, uint64_t offset, double *out, int64_t n,
                            void *stream);

@@ -459,11 +459,23 @@ EXPORT void orc_gbm_paths(double mu, double sigma, double x0, double t_end, int 
 }
 
 /* CIR truncated Euler (mlmc.py:289-331), exact-Gaussian and table sides. */
-EXPORT void orc_cir_euler_paths(double kappa, double theta, double sigma, double x0, double t_end,
-                                int level, int n0, int payoff_call, double strike,
-                                const double *coeffs, int degree, int64_t K1, uint64_t seed,
-                                uint64_t seq, int64_t n_paths, int64_t path_lo, int64_t path_hi,
-                                double *pf_e, double *pc_e, double *pf_a, double *pc_a) {
+static double cir_step1(double x, double dw, double dt, double kappa, double theta, double sigma, int milstein) {
+    double r = x + kappa * (theta - x) * dt + sigma * sqrt(fabs(x)) * dw; /* mlmc.py:295-296 */
+    if (milstein) r = r + 0.25 * sigma * sigma * (dw * dw - dt);
+    return r;
+}
+
+/* CIR truncated Euler (mlmc.py:289-331, step :295-296) and, with milstein
+ * = 1, the truncated Milstein scheme the reference does not have (BASELINE
+ * config 5 "CIR ... with Milstein"): the Euler step plus the Milstein term
+ * 1/2 b b' (dW^2 - dt) of b(x) = sigma sqrt(x), i.e. sigma^2/4 (dW^2 - dt),
+ * added last; the device scheme is cir_step<true> (arv_mlmc.cu).  Same
+ * coupling, uniforms and payoffs as the Euler loop. */
+EXPORT void orc_cir_paths(double kappa, double theta, double sigma, double x0, double t_end,
+                          int level, int n0, int milstein, int payoff_call, double strike,
+                          const double *coeffs, int degree, int64_t K1, uint64_t seed,
+                          uint64_t seq, int64_t n_paths, int64_t path_lo, int64_t path_hi,
+                          double *pf_e, double *pc_e, double *pf_a, double *pc_a) {
     uint64_t s0, inc, AN, CN;
     orc_pcg32_seed(seed, seq, &s0, &inc);
     orc_lcg_jump((uint64_t)n_paths, inc, &AN, &CN);
@@ -471,7 +483,7 @@ EXPORT void orc_cir_euler_paths(double kappa, double theta, double sigma, double
     const double dt_f = t_end / (double)n_f;
     const double dt_c = 2.0 * dt_f;
     const double sq_f = sqrt(dt_f);
-#define CIR_EM(x, dw, dt) ((x) + kappa * (theta - (x)) * (dt) + sigma * sqrt(fabs(x)) * (dw))
+#define CIR_EM(x, dw, dt) cir_step1(x, dw, dt, kappa, theta, sigma, milstein)
     for (int64_t p = path_lo; p < path_hi; ++p) {
         uint64_t A, C, s;
         orc_lcg_jump((uint64_t)p, inc, &A, &C);
@@ -508,6 +520,15 @@ EXPORT void orc_cir_euler_paths(double kappa, double theta, double sigma, double
         pc_a[i] = ca;
     }
 #undef CIR_EM
+}
+
+EXPORT void orc_cir_euler_paths(double kappa, double theta, double sigma, double x0, double t_end,
+                                int level, int n0, int payoff_call, double strike,
+                                const double *coeffs, int degree, int64_t K1, uint64_t seed,
+                                uint64_t seq, int64_t n_paths, int64_t path_lo, int64_t path_hi,
+                                double *pf_e, double *pc_e, double *pf_a, double *pc_a) {
+    orc_cir_paths(kappa, theta, sigma, x0, t_end, level, n0, 0, payoff_call, strike, coeffs, degree, K1, seed,
+                  seq, n_paths, path_lo, path_hi, pf_e, pc_e, pf_a, pc_a);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -74,6 +74,8 @@ _sig("orc_gbm_paths", _dbl, _dbl, _dbl, _dbl, _int, _int, _int, _int, _dbl, _p, 
      _u64, _u64, _i64, _i64, _i64, _p, _p, _p, _p)
 _sig("orc_cir_euler_paths", _dbl, _dbl, _dbl, _dbl, _dbl, _int, _int, _int, _dbl, _p, _int, _i64,
      _u64, _u64, _i64, _i64, _i64, _p, _p, _p, _p)
+_sig("orc_cir_paths", _dbl, _dbl, _dbl, _dbl, _dbl, _int, _int, _int, _int, _dbl, _p, _int, _i64,
+     _u64, _u64, _i64, _i64, _i64, _p, _p, _p, _p)
 
 
 _sig("orc_philox_words", _u64, _u64, _u64, _i64, _p)
@@ -292,14 +294,16 @@ def gbm_paths(*, mu, sigma, x0, t_end, level, n0, milstein, payoff_call, strike,
 
 
 def cir_euler_paths(*, kappa, theta, sigma, x0, t_end, level, n0, payoff_call, strike, coeffs,
-                    seed, seq, n_paths, path_lo=0, path_hi=None):
+                    seed, seq, n_paths, path_lo=0, path_hi=None, milstein=False):
+    """CIR truncated Euler (mlmc.py:289-331) or, milstein=True, the truncated
+    Milstein restatement (orc_cir_paths in oracle.c; no reference scheme)."""
     path_hi = n_paths if path_hi is None else path_hi
     coeffs = _c(coeffs, np.float64)
     m = path_hi - path_lo
     outs = [np.empty(m) for _ in range(4)]
-    lib.orc_cir_euler_paths(kappa, theta, sigma, x0, t_end, level, n0, int(payoff_call), strike,
-                            _ptr(coeffs), coeffs.shape[0] - 1, coeffs.shape[1], seed, seq, n_paths,
-                            path_lo, path_hi, *[_ptr(o) for o in outs])
+    lib.orc_cir_paths(kappa, theta, sigma, x0, t_end, level, n0, int(milstein), int(payoff_call), strike,
+                      _ptr(coeffs), coeffs.shape[0] - 1, coeffs.shape[1], seed, seq, n_paths,
+                      path_lo, path_hi, *[_ptr(o) for o in outs])
     return tuple(outs)
 
 

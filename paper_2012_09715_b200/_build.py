@@ -10,6 +10,7 @@ travels to the GPU box with the repository snapshot.
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import shutil
 import subprocess
@@ -43,12 +44,27 @@ def sources() -> list[str]:
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def _deps() -> list[str]:
+    return sorted(sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h")))
+
+
+def source_hash() -> str:
+    """sha256 over the library's sources and build flags (embedded in the
+    library as arv_source_hash(); a mismatch at load time = stale library)."""
+    h = hashlib.sha256()
+    for p in _deps():
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as fh:
+            h.update(fh.read())
+    h.update(repr((ARCH_FLAGS, PER_FILE_FLAGS)).encode())
+    return h.hexdigest()
+
+
 def needs_build() -> bool:
     if not os.path.exists(LIB_PATH):
         return True
     t = os.path.getmtime(LIB_PATH)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h"))
-    return any(os.path.getmtime(p) > t for p in deps)
+    return any(os.path.getmtime(p) > t for p in _deps())
 
 
 def build(verbose_ptxas: bool = False, force: bool = False, defines=(), out: str | None = None) -> str:
@@ -62,10 +78,14 @@ def build(verbose_ptxas: bool = False, force: bool = False, defines=(), out: str
     common = ARCH_FLAGS + [
         "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
         "-I", INCLUDE, "-I", CSRC, "--expt-relaxed-constexpr",
+        # a misplaced `#pragma unroll` (warning 609-D) once silently dropped the
+        # tuned unroll of the generators: every nvcc / ptxas warning fails the build
+        "-Werror", "all-warnings",
     ]
     if verbose_ptxas:
         common += ["-Xptxas", "-v"]
     common += [f"-D{d}" for d in defines]
+    common += [f'-DARV_SOURCE_HASH="{source_hash()}"']
     if defines or out is not None:  # experiment variants: objects outside the repo
         objdir = os.path.join(tempfile.gettempdir(), "arv_variant_build", os.path.basename(target))
         os.makedirs(objdir, exist_ok=True)

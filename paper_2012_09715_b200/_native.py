@@ -38,6 +38,7 @@ PHILOX_UNIFORM, PHILOX_CONSTANT, PHILOX_DYADIC, PHILOX_GAUSSIAN = range(4)
 _SIGNATURES = {
     "arv_abi_version": ([], _int),
     "arv_last_error": ([], C.c_char_p),
+    "arv_source_hash": ([], C.c_char_p),
     "arv_launch_count": ([], _u64),
     "arv_constant_eval": ([_p, _i64, _p, _p, _i64, _p], _int),
     "arv_dyadic_index": ([_p, _i64, _i64, _p, _p], _int),
@@ -52,6 +53,7 @@ _SIGNATURES = {
     "arv_pcg32_uniform_f32": ([_u64, _u64, _u64, _p, _i64, _p], _int),
     "arv_pcg32_constant_f32": ([_u64, _u64, _u64, _p, _int, _p, _i64, _p], _int),
     "arv_pcg32_subdyadic_f32": ([_u64, _u64, _u64, _p, _int, _int, _int, _p, _i64, _p], _int),
+    "arv_lattice_subdyadic_f32": ([_p, _int, _int, _int, _int, _p, _p, _p], _int),
     "arv_pcg32_gaussian_f64": ([_u64, _u64, _u64, _p, _i64, _p], _int),
     "arv_pcg32_gaussian_f32": ([_u64, _u64, _u64, _p, _i64, _p], _int),
     "arv_philox_words": ([_u64, _u64, _u64, _p, _i64, _p], _int),
@@ -71,13 +73,28 @@ _SIGNATURES = {
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
 
+def _built_hash(path: str) -> str | None:
+    """arv_source_hash() of a built library, read from the file (the string is
+    tagged "ARV_SOURCE_HASH=<hex>" in .rodata) without loading it."""
+    import re
+
+    with open(path, "rb") as fh:
+        m = re.search(rb"ARV_SOURCE_HASH=([0-9a-f]{64}|unknown)", fh.read())
+    return m.group(1).decode() if m else None
+
+
 def _load() -> C.CDLL:
     # ARV_LIB_PATH: an alternative build of the same library (tuning experiments only)
-    path = os.environ.get("ARV_LIB_PATH") or _build.LIB_PATH
-    if not os.path.exists(path):
-        if os.environ.get("ARV_NO_AUTOBUILD"):
-            raise ImportError(f"{path} is missing; run `python -m paper_2012_09715_b200._build`")
-        _build.build()
+    alt = os.environ.get("ARV_LIB_PATH")
+    path = alt or _build.LIB_PATH
+    if not alt:
+        stale = not os.path.exists(path) or _built_hash(path) != _build.source_hash()
+        if stale:
+            # a library built from other sources must never load silently
+            if os.environ.get("ARV_NO_AUTOBUILD"):
+                raise ImportError(f"{path} is missing or was built from other sources; "
+                                  "run `python -m paper_2012_09715_b200._build`")
+            _build.build(force=True)
     lib = C.CDLL(path)
     for name, (args, res) in _SIGNATURES.items():
         fn = getattr(lib, name)  # AttributeError = stale or broken library: fail loudly

@@ -121,6 +121,13 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
     return v;
 }
 
+// ld.shared.v2.f32 (LDS.64) at a shared-space byte address.
+__device__ __forceinline__ float2 lds_f32x2(uint32_t addr) {
+    float2 v;
+    asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+
 // XSH-RR output of a state (the value produced *before* stepping).
 __device__ __forceinline__ uint32_t pcg32_output(uint64_t old) {
     const uint32_t lo = static_cast<uint32_t>(old);
@@ -536,7 +543,10 @@ __device__ __forceinline__ float as241_f32(float u) {
 }
 
 // ------------------------------------------------- dyadic index helpers --
-// _kernels.pyx:36 / :51 (exponent bits), with a memory-safety clamp at 0.
+// _kernels.pyx:36 / :51 (exponent bits), capped at `cap` like the reference.
+// There is no lower clamp here: u > 1/2 or u = 1 gives a negative index
+// (dyadic_index32(1.0) = -1 in the reference), so callers that index a table
+// with the result clamp it at 0 themselves.
 __device__ __forceinline__ long long dyadic_idx64(double v, long long cap) {
     const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
     const long long idx = 1022 - static_cast<long long>(bits >> 52);

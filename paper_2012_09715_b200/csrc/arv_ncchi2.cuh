@@ -359,8 +359,14 @@ __device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, do
     double inv_w;
     // bulk solves: the first sweep only places the Taylor step (6-sigma window);
     // the verification and any further sweeps use the full window
-    NcCdf c = L.blocked && ARV_NC_NARROW_START ? ncchi2_cdf_sweep<true, true>(a0, x, L, u, inv_w)
-                                               : ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w);
+    const bool narrow = L.blocked && ARV_NC_NARROW_START;
+    NcCdf c = narrow ? ncchi2_cdf_sweep<true, true>(a0, x, L, u, inv_w) : ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w);
+    if (narrow && fabs(c.resid) <= tol_f) {
+        // The narrow window truncates ~1e-11..1e-10, about tol_f: never accept
+        // (or bracket on) its residual -- re-evaluate on the full window.
+        const NcCdf f = ncchi2_cdf_sweep<false>(a0, x, L, u, inv_w);
+        c = fabs(f.resid) <= tol_f ? f : ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w);
+    }
 #if ARV_NC_COUNT
     int n_eval = 1;
 #endif

@@ -68,6 +68,15 @@ int resident_ctas(const void *fn, int block, size_t smem) {
 extern "C" {
 
 int arv_abi_version(void) { return ARV_ABI_VERSION; }
+// sha256 of the csrc/ and include/ sources this library was built from
+// (_build.source_hash(), passed as -DARV_SOURCE_HASH): the loader rebuilds or
+// refuses a library whose sources changed since (_native._load).
+#ifndef ARV_SOURCE_HASH
+#define ARV_SOURCE_HASH "unknown"
+#endif
+// The tagged string is also read from the file itself (no dlopen needed).
+static const char kSourceHashTag[] = "ARV_SOURCE_HASH=" ARV_SOURCE_HASH;
+const char *arv_source_hash(void) { return kSourceHashTag + 16; }
 const char *arv_last_error(void) { return arv::g_err; }
 uint64_t arv_launch_count(void) { return arv::g_launches.load(std::memory_order_relaxed); }
 

@@ -14,6 +14,8 @@
 //   constant   values[floor(2^q u)]            (_kernels.pyx:16-23)
 //   subdyadic  octave x sub-interval Horner    (_kernels.pyx:76-93 when sub_bits = 0)
 //   uniform    u itself; gaussian32/64 = AS241 (exact_dist.py:87-126)
+#include <algorithm>
+
 #include "arv_common.cuh"
 
 namespace arv {
@@ -133,14 +135,13 @@ __device__ __forceinline__ void eval_two(const Eval &eval, uint32_t w0, uint32_t
     }
 }
 
-// Drive `eval(w) -> uint32 bits` over the call's samples with G-wide stores
-// (out must be 4*G-byte aligned).
+// The group loop: thread g0 starts at state `s` (its first group) and
+// produces its groups with G-wide stores (out must be 4*G-byte aligned).
 template <int G, class Eval>
-__device__ __forceinline__ void gen_loop_vec(const GenArgs &a, uint32_t *__restrict__ out, const Eval &eval) {
+__device__ __forceinline__ void gen_run(const GenArgs &a, uint32_t *__restrict__ out, const Eval &eval, uint64_t s,
+                                        uint64_t g0) {
     const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t n_full = static_cast<uint64_t>(a.n) / G;
-    uint64_t s = group_start(a, g0);
     const uint64_t z = static_cast<uint64_t>(threadIdx.x) * a.zero;  // 0, but not provably uniform
     const uint64_t inc = a.inc + z;
     const Affine st{a.stride.a + z, a.stride.c + z};
@@ -151,12 +152,6 @@ __device__ __forceinline__ void gen_loop_vec(const GenArgs &a, uint32_t *__restr
     uint32_t *p = out + G * g0;
     const uint64_t step = G * T;
 #pragma unroll kGenUnroll
-#if ARV_GEN_PDL
-    // Programmatic dependent launch: the prologue above (table staging, start
-    // state) may overlap the previous kernel's tail on the stream; wait for it
-    // to complete (and its stores to be visible) before storing.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
     for (uint32_t it = 0; it < iters; ++it) {
         uint32_t w[G];
 #pragma unroll
@@ -180,15 +175,43 @@ __device__ __forceinline__ void gen_loop_vec(const GenArgs &a, uint32_t *__restr
     }
 }
 
+__device__ __forceinline__ void pdl_wait() {
+#if ARV_GEN_PDL
+    // Programmatic dependent launch: everything before this may overlap the
+    // previous kernel's tail on the stream; wait for it to complete (and its
+    // stores to be visible) before reading a table or storing.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+// Drive `eval(w) -> uint32 bits` over the call's samples with G-wide stores.
+// `stage()` runs after griddepcontrol.wait and before the first store: it
+// stages the kernel's table into shared memory, so a table written by the
+// previous kernel on the stream is visible (PDL RAW ordering).  Only the
+// parameter-only start-state walk overlaps the predecessor's tail.
+template <int G, class Eval, class Stage>
+__device__ __forceinline__ void gen_loop_vec(const GenArgs &a, uint32_t *__restrict__ out, const Eval &eval,
+                                             const Stage &stage) {
+    const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t s = group_start(a, g0);
+    pdl_wait();
+    stage();
+    gen_run<G>(a, out, eval, s, g0);
+}
+
 // Scalar-store variant for outputs that are not 16-byte aligned.
-template <class Eval>
+template <class Eval, class Stage>
 __device__ __forceinline__ void gen_loop_v1(uint64_t s_base, uint64_t inc, int64_t n, uint32_t *__restrict__ out,
-                                            const Eval &eval) {
+                                            const Eval &eval, const Stage &stage) {
     const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const Affine j0 = lcg_jump(i, inc);
     const Affine sT = lcg_jump(T, inc);
     uint64_t s = j0.a * s_base + j0.c;
+#if ARV_GEN_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+    stage();
     for (; i < static_cast<uint64_t>(n); i += T) {
         out[i] = eval(pcg32_output(s));
         s = lcg_step(s, sT.a, sT.c);
@@ -196,10 +219,14 @@ __device__ __forceinline__ void gen_loop_v1(uint64_t s_base, uint64_t inc, int64
 }
 
 // MODE: 1 = scalar stores (unaligned out), 4 = v4, 8 = v8.
-template <int MODE, class Eval>
-__device__ __forceinline__ void gen_dispatch(const GenArgs &a, uint32_t *out, const Eval &ev) {
-    if constexpr (MODE == 1) gen_loop_v1(a.s_base, a.inc, a.n, out, ev);
-    else gen_loop_vec<MODE>(a, out, ev);
+struct NoStage {
+    __device__ __forceinline__ void operator()() const {}
+};
+template <int MODE, class Eval, class Stage = NoStage>
+__device__ __forceinline__ void gen_dispatch(const GenArgs &a, uint32_t *out, const Eval &ev,
+                                             const Stage &stage = Stage{}) {
+    if constexpr (MODE == 1) gen_loop_v1(a.s_base, a.inc, a.n, out, ev, stage);
+    else gen_loop_vec<MODE>(a, out, ev, stage);
 }
 
 // ------------------------------------------------------------ evaluators --
@@ -329,6 +356,90 @@ __device__ __forceinline__ void stage_subdyadic(float *sm, const float *__restri
     __syncthreads();
 }
 
+// Degree-1 octave x sub-interval evaluator with the reflection's sign folded
+// into the table ("signed lattice table"), bit-identical to EvalSubDyadic<1>.
+//   i  = (int32)w >> 9 (the lattice index k = w >> 9 less 2^23 when u >= 1/2),
+//   g  = as_float(0x4B400000 + i) = 12582912 + i   (one LEA.HI.SX32),
+//   vh = (g - 12582912) + 1/2 = i + 1/2            (two exact FADD2 per pair).
+// For u < 1/2, vh = u 2^23 > 0; for u >= 1/2, vh = (u - 1) 2^23 = -(1 - u) 2^23,
+// so |vh| = v 2^23 with v = min(u, 1 - u) and sign(vh) is the reference's
+// predicate.  The table is indexed by bits(vh) >> (23 - b) = s|E|sub: entry
+// (c0, c1 2^-23) for vh > 0 and (-c0, c1 2^-23) for vh < 0, so
+//   RN(RN(c1' vh) + c0') = RN(c0 + RN(c1 v))  (vh > 0)
+//                        = -RN(c0 + RN(c1 v)) (vh < 0; RN is odd-symmetric)
+// exactly the reference's separately rounded z = c1 v + c0 and its sign flip,
+// with no reflection, no sign fix-up and one LDS.64 per sample.  Two
+// conditions make it exact, both checked per table entry while staging
+// (stage_linsigned): c1 2^-23 is exact (no subnormal rounding), and no lattice
+// point of the entry gives z == 0 (the reference returns -0.0 there, the
+// signed table +0.0).  If either fails the kernel runs EvalSubDyadic<1>.
+constexpr int kSignedE0 = 126;  // exponent of |vh| = 1/2 (octave 23)
+
+struct EvalLinSigned {
+    uint32_t base;   // shared byte address of the float2 table, pre-offset by -8 (126 << b)
+    int shift;       // 23 - b
+    uint32_t eight;  // 8 in a register: the address is one IMAD
+    __device__ __forceinline__ static uint32_t magic(uint32_t w) {
+        return 0x4B400000u + static_cast<uint32_t>(static_cast<int32_t>(w) >> 9);  // LEA.HI.SX32
+    }
+    __device__ __forceinline__ uint32_t operator()(uint32_t w) const {
+        const float vh = __fadd_rn(__fadd_rn(__uint_as_float(magic(w)), -12582912.0f), 0.5f);
+        const float2 c = lds_f32x2(mad_u32(__float_as_uint(vh) >> shift, eight, base));
+        return __float_as_uint(__fadd_rn(__fmul_rn(c.y, vh), c.x));
+    }
+    static constexpr bool kHasPair = true;
+    __device__ __forceinline__ void pair(uint32_t w0, uint32_t w1, uint32_t &r0, uint32_t &r1) const {
+        const uint64_t g = pack2(magic(w0), magic(w1));
+        const uint64_t vh = f32x2_add(f32x2_add(g, kMinusMagic2), kHalf2);
+        const float2 c0 = lds_f32x2(mad_u32(lo32(vh) >> shift, eight, base));
+        const float2 c1 = lds_f32x2(mad_u32(hi32(vh) >> shift, eight, base));
+        r0 = __float_as_uint(__fadd_rn(__fmul_rn(c0.y, __uint_as_float(lo32(vh))), c0.x));
+        r1 = __float_as_uint(__fadd_rn(__fmul_rn(c1.y, __uint_as_float(hi32(vh))), c1.x));
+    }
+    static constexpr uint64_t kMinusMagic2 = 0xCB400000CB400000ull;  // {-12582912, -12582912}
+    static constexpr uint64_t kHalf2 = 0x3F0000003F000000ull;        // {0.5, 0.5}
+};
+
+// Shared bytes of the signed table for sub_bits b: entries [0, 23 << b) for
+// vh > 0 and the same at +2^(8+b) for vh < 0 (bit 31 of bits(vh)).
+__host__ __device__ constexpr int linsigned_entries(int b) { return (1 << (8 + b)) + (23 << b); }
+
+// z = RN(RN(c1 v) + c0) in f32 at lattice point v = (m + 1/2) 2^-23.
+__device__ __forceinline__ float lin_at(float c0, float c1, int64_t m) {
+    const float v = __fmul_rn(static_cast<float>(m) + 0.5f, 0x1p-23f);  // exact (m < 2^22)
+    return __fadd_rn(__fmul_rn(c1, v), c0);
+}
+
+// Stage natural-layout coeffs (2, K, 2^b) into the signed table; returns the
+// CTA-wide verdict that the signed evaluation is bit-exact for this table.
+__device__ __forceinline__ bool stage_linsigned(float2 *sm, const float *__restrict__ coeffs, int K, int b) {
+    const int nsub = 1 << b;
+    const int neg = 1 << (8 + b);
+    bool ok = true;
+    for (int e = threadIdx.x; e < (23 << b); e += blockDim.x) {
+        const int E = kSignedE0 + (e >> b), sub = e & (nsub - 1);
+        const int j = 149 - E;  // octave 1..23
+        const int jj = j < K ? j : K;
+        const int ss = j < K ? sub : 0;
+        const float c0 = __ldg(coeffs + static_cast<int64_t>(jj - 1) * nsub + ss);
+        const float c1 = __ldg(coeffs + (static_cast<int64_t>(K) + jj - 1) * nsub + ss);
+        const float c1s = __fmul_rn(c1, 0x1p-23f);
+        ok &= isfinite(c0) && isfinite(c1) && __fmul_rn(c1s, 0x1p23f) == c1;
+        // lattice points |vh| = m + 1/2 inside [lo, hi) of this entry
+        const float lo = __uint_as_float(static_cast<uint32_t>(E) << 23 | static_cast<uint32_t>(sub) << (23 - b));
+        const float hi = __uint_as_float((static_cast<uint32_t>(E) << 23) + (static_cast<uint32_t>(sub + 1) << (23 - b)));
+        const int64_t m_lo = static_cast<int64_t>(ceilf(lo - 0.5f));
+        const int64_t m_hi = static_cast<int64_t>(ceilf(hi - 0.5f)) - 1;
+        if (m_lo <= m_hi) {  // z is monotone in v over the entry: check the ends
+            const float za = lin_at(c0, c1, m_lo), zb = lin_at(c0, c1, m_hi);
+            ok &= (za > 0.0f && zb > 0.0f) || (za < 0.0f && zb < 0.0f);
+        }
+        sm[e] = make_float2(c0, c1s);
+        sm[neg + e] = make_float2(-c0, c1s);
+    }
+    return __syncthreads_and(ok) != 0;
+}
+
 // --------------------------------------------------------------- kernels --
 template <int MODE, class Eval>
 __global__ void __launch_bounds__(256, ARV_GEN_MINB) k_gen_simple(GenArgs a, uint32_t *out, Eval eval) {
@@ -343,10 +454,11 @@ __global__ void __launch_bounds__(256, ARV_GEN_MINB) k_pcg32_constant(GenArgs a,
         extern __shared__ float4 smem4[];
         float *sm = reinterpret_cast<float *>(smem4);
         const int nv = 1 << q;
-        for (int i = threadIdx.x; i < nv; i += blockDim.x) sm[i] = __ldg(values + i);
-        __syncthreads();
         const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
-        gen_dispatch<MODE>(a, out, EvalConstantSmem{base, 32 - q, 4u + threadIdx.x * a.zero32});
+        gen_dispatch<MODE>(a, out, EvalConstantSmem{base, 32 - q, 4u + threadIdx.x * a.zero32}, [&] {
+            for (int i = threadIdx.x; i < nv; i += blockDim.x) sm[i] = __ldg(values + i);
+            __syncthreads();
+        });
     } else if constexpr (KIND == 1) {
         gen_dispatch<MODE>(a, out, EvalConstantGlobal{values, 32 - q});
     } else {
@@ -362,9 +474,63 @@ __global__ void __launch_bounds__(256, ARV_GEN_MINB) k_pcg32_subdyadic(GenArgs a
     asm volatile("griddepcontrol.launch_dependents;");
 #endif
     __shared__ float sm[(DEG + 1) * kLatticePlane];
-    stage_subdyadic<DEG>(sm, coeffs, K, b);
     const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sm)) - 4u * (kLatticeE0 << b);
-    gen_dispatch<MODE>(a, out, EvalSubDyadic<DEG>{base, 23 - b, 4u + threadIdx.x * a.zero32});
+    // the table is staged after griddepcontrol.wait (see gen_loop_vec)
+    gen_dispatch<MODE>(a, out, EvalSubDyadic<DEG>{base, 23 - b, 4u + threadIdx.x * a.zero32},
+                       [&] { stage_subdyadic<DEG>(sm, coeffs, K, b); });
+}
+
+// Degree-1 sub-interval generator on the signed table (EvalLinSigned), with
+// EvalSubDyadic<1> as the exact fallback for tables that fail its checks.
+template <int MODE>
+__global__ void __launch_bounds__(256, ARV_GEN_MINB) k_pcg32_linsigned(GenArgs a, const float *__restrict__ coeffs, int K,
+                                                                      int b, uint32_t *out) {
+    static_assert(MODE == 4 || MODE == 8, "vector stores only");
+#if ARV_GEN_PDL
+    asm volatile("griddepcontrol.launch_dependents;");
+#endif
+    extern __shared__ float4 smem4[];
+    const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t s = group_start(a, g0);
+    pdl_wait();
+    float2 *tab = reinterpret_cast<float2 *>(smem4);
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
+    if (stage_linsigned(tab, coeffs, K, b)) {
+        gen_run<MODE>(a, out, EvalLinSigned{sbase - 8u * (kSignedE0 << b), 23 - b, 8u + threadIdx.x * a.zero32}, s, g0);
+    } else {  // CTA-uniform
+        float *sm = reinterpret_cast<float *>(smem4);
+        __syncthreads();
+        stage_subdyadic<1>(sm, coeffs, K, b);
+        gen_run<MODE>(a, out, EvalSubDyadic<1>{sbase - 4u * (kLatticeE0 << b), 23 - b, 4u + threadIdx.x * a.zero32}, s,
+                      g0);
+    }
+}
+
+// Test hook: every point of the f32 lattice through the generators'
+// evaluators (same structs, same staging), out[k] = eval(w), w >> 9 == k.
+// The low 9 bits of w are set to a hash of k: the evaluators must ignore them.
+constexpr int kLatticeN = 1 << 23;
+template <int MODE>
+__global__ void __launch_bounds__(256) k_lattice_sub(const float *__restrict__ coeffs, int K, int b, uint32_t *out,
+                                                     int *fast) {
+    extern __shared__ float4 smem4[];
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem4));
+    const int stride = gridDim.x * blockDim.x;
+    const int k0 = blockIdx.x * blockDim.x + threadIdx.x;
+    bool use_signed = false;
+    if constexpr (MODE == 1) {
+        use_signed = stage_linsigned(reinterpret_cast<float2 *>(smem4), coeffs, K, b);
+        if (fast && blockIdx.x == 0 && threadIdx.x == 0) *fast = use_signed ? 1 : 0;
+    }
+    if (use_signed) {
+        const EvalLinSigned ev{sbase - 8u * (kSignedE0 << b), 23 - b, 8u};
+        for (int k = k0; k < kLatticeN; k += stride) out[k] = ev((static_cast<uint32_t>(k) << 9) | ((k * 0x9E3779B1u) >> 23));
+        return;
+    }
+    __syncthreads();
+    stage_subdyadic<1>(reinterpret_cast<float *>(smem4), coeffs, K, b);
+    const EvalSubDyadic<1> ev{sbase - 4u * (kLatticeE0 << b), 23 - b, 4u};
+    for (int k = k0; k < kLatticeN; k += stride) out[k] = ev((static_cast<uint32_t>(k) << 9) | ((k * 0x9E3779B1u) >> 23));
 }
 
 // f64 exact comparator: groups of 4 samples, two 16-byte stores.
@@ -465,13 +631,25 @@ static int launch_simple(uint64_t seed, uint64_t sid, uint64_t offset, uint32_t 
     return check_launch(what);
 }
 
+// Degree 1 with b <= kSignedMaxBits runs the signed-table kernel (b = 5
+// would need 71 KB of shared memory per CTA).
+#ifndef ARV_GEN_SIGNED
+#define ARV_GEN_SIGNED 1
+#endif
+constexpr int kSignedMaxBits = 4;
+
 template <int D>
 static void launch_subdyadic(uint64_t seed, uint64_t sid, uint64_t offset, const float *coeffs, int K, int sub_bits,
                              float *out, int64_t n, int mode, void *stream) {
-    const void *fn = mode == 8   ? (const void *)k_pcg32_subdyadic<D, 8>
+    const bool signed_tab = ARV_GEN_SIGNED && D == 1 && mode != 1 && sub_bits <= kSignedMaxBits;
+    const void *fn = signed_tab  ? (mode == 8 ? (const void *)k_pcg32_linsigned<8> : (const void *)k_pcg32_linsigned<4>)
+                     : mode == 8 ? (const void *)k_pcg32_subdyadic<D, 8>
                      : mode == 4 ? (const void *)k_pcg32_subdyadic<D, 4>
                                  : (const void *)k_pcg32_subdyadic<D, 1>;
-    const int grid = gen_grid(fn, n, mode);
+    const size_t smem = signed_tab ? std::max<size_t>(sizeof(float2) * linsigned_entries(sub_bits),
+                                                      sizeof(float) * 2 * kLatticePlane)
+                                   : 0;
+    const int grid = gen_grid(fn, n, mode, smem);
     const int64_t T = static_cast<int64_t>(grid) * kGenBlock;
     const GenArgs a = make_gen_args(seed, sid, offset, n, T, mode == 1 ? 4 : mode);
     uint32_t *o = reinterpret_cast<uint32_t *>(out);
@@ -481,18 +659,25 @@ static void launch_subdyadic(uint64_t seed, uint64_t sid, uint64_t offset, const
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(kGenBlock);
-        cfg.dynamicSmemBytes = 0;
+        cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (mode == 8) cudaLaunchKernelEx(&cfg, k_pcg32_subdyadic<D, 8>, a, coeffs, K, sub_bits, o);
+        if (signed_tab && mode == 8) cudaLaunchKernelEx(&cfg, k_pcg32_linsigned<8>, a, coeffs, K, sub_bits, o);
+        else if (signed_tab) cudaLaunchKernelEx(&cfg, k_pcg32_linsigned<4>, a, coeffs, K, sub_bits, o);
+        else if (mode == 8) cudaLaunchKernelEx(&cfg, k_pcg32_subdyadic<D, 8>, a, coeffs, K, sub_bits, o);
         else cudaLaunchKernelEx(&cfg, k_pcg32_subdyadic<D, 4>, a, coeffs, K, sub_bits, o);
         return;
     }
 #endif
+    if (signed_tab) {
+        if (mode == 8) k_pcg32_linsigned<8><<<grid, kGenBlock, smem, s>>>(a, coeffs, K, sub_bits, o);
+        else k_pcg32_linsigned<4><<<grid, kGenBlock, smem, s>>>(a, coeffs, K, sub_bits, o);
+        return;
+    }
     if (mode == 8) k_pcg32_subdyadic<D, 8><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o);
     else if (mode == 4) k_pcg32_subdyadic<D, 4><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o);
     else k_pcg32_subdyadic<D, 1><<<grid, kGenBlock, 0, s>>>(a, coeffs, K, sub_bits, o);
@@ -579,6 +764,25 @@ int arv_pcg32_subdyadic_f32(uint64_t seed, uint64_t stream_id, uint64_t offset, 
     }
     note_launch();
     return check_launch("arv_pcg32_subdyadic_f32");
+}
+
+int arv_lattice_subdyadic_f32(const float *coeffs, int degree, int K, int sub_bits, int mode, float *out, int *fast,
+                              void *stream) {
+    if (degree != 1) return set_error(ARV_ERR_CONFIG, "lattice hook: degree must be 1");
+    if (K < 1 || K > 40) return set_error(ARV_ERR_CONFIG, "octave count K must be in [1, 40], got %d", K);
+    if (sub_bits < 0 || sub_bits > (mode == 1 ? kSignedMaxBits : 5))
+        return set_error(ARV_ERR_CONFIG, "sub_bits out of range for mode %d", mode);
+    const size_t smem = std::max<size_t>(sizeof(float2) * linsigned_entries(sub_bits), sizeof(float) * 2 * kLatticePlane);
+    cudaStream_t s = as_stream(stream);
+    uint32_t *o = reinterpret_cast<uint32_t *>(out);
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute((const void *)k_lattice_sub<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute((const void *)k_lattice_sub<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    if (mode == 1) k_lattice_sub<1><<<4 * device_sm_count(), 256, smem, s>>>(coeffs, K, sub_bits, o, fast);
+    else k_lattice_sub<0><<<4 * device_sm_count(), 256, smem, s>>>(coeffs, K, sub_bits, o, fast);
+    note_launch();
+    return check_launch("arv_lattice_subdyadic_f32");
 }
 
 int arv_pcg32_gaussian_f64(uint64_t seed, uint64_t stream_id, uint64_t offset, double *out, int64_t n, void *stream) {

@@ -311,8 +311,12 @@ class Pcg32Stream:
         if out is None:
             out = torch.empty(n, dtype=torch.float32, pin_memory=True)
         if not isinstance(out, torch.Tensor):
-            host = out
-            out = torch.from_numpy(np.ascontiguousarray(host))
+            host = np.asarray(out)
+            # a non-contiguous or read-only array would be filled through a
+            # temporary copy and the caller's buffer never written: refuse it
+            if not (host.flags.c_contiguous and host.flags.writeable):
+                raise ConfigError("out must be a C-contiguous, writeable float32 array")
+            out = torch.from_numpy(host)
         if out.numel() != n or out.dtype != torch.float32 or out.is_cuda:
             raise ConfigError("out must be a host float32 buffer of n elements")
         chunk = max(4, min(chunk, n)) & ~3

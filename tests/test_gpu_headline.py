@@ -1,0 +1,164 @@
+"""GPU parity of the headline generator (config 2) beyond sampled chunks:
+
+* the evaluators of the fused generators over the WHOLE f32 lattice (all 2^23
+  values of w >> 9), for the shipped tables and random tables at every
+  sub_bits the signed-table kernel takes, against the oracle;
+* the signed-table kernel's exactness checks and its fallback (a table with
+  an exact zero on the lattice, where the reference returns -0.0; a slope
+  whose 2^-23 scaling is inexact);
+* the full 2^28-sample config-2 output against the oracle's sha256;
+* programmatic-dependent-launch ordering: a table written by the kernel that
+  runs immediately before the generator on the stream is the one used.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+LATTICE = 1 << 23
+
+
+def bits(a):
+    if isinstance(a, torch.Tensor):
+        a = a.cpu().numpy()
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+@pytest.fixture(scope="module")
+def arv():
+    import paper_2012_09715_b200 as arv
+
+    return arv
+
+
+@pytest.fixture(scope="module")
+def lattice_u():
+    k = np.arange(LATTICE, dtype=np.float64)
+    return ((k + 0.5) * 2.0**-23).astype(np.float32)
+
+
+def lattice_eval(coeffs, sub_bits, mode):
+    from paper_2012_09715_b200 import _device as dev
+    from paper_2012_09715_b200._native import call
+
+    c = torch.from_numpy(np.ascontiguousarray(coeffs, dtype=np.float32)).cuda()
+    out = torch.empty(LATTICE, dtype=torch.float32, device="cuda")
+    fast = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    call("arv_lattice_subdyadic_f32", c.data_ptr(), coeffs.shape[0] - 1, coeffs.shape[1], sub_bits, mode,
+         out.data_ptr(), fast.data_ptr(), dev.stream_handle())
+    return out.cpu().numpy(), int(fast.item())
+
+
+def random_table(rng, K, b):
+    """Degree-1 table shaped like a lower-tail ICDF fit: c1 > 0, z < 0 on (0, 1/2)."""
+    c1 = rng.uniform(0.5, 40.0, size=(K, 1 << b))
+    c0 = -(0.5 * c1) - rng.uniform(1e-3, 3.0, size=(K, 1 << b))
+    return np.stack([c0, c1]).astype(np.float32)
+
+
+@pytest.mark.parametrize("name,b", [("subdyadic_linear_k16_s8", 3), ("dyadic_linear_k15", 0)])
+def test_shipped_tables_whole_lattice(arv, orc, tables_npz, lattice_u, name, b):
+    if name == "dyadic_linear_k15":  # reference layout -> natural (2, K, 1): octave j -> ref[:, j]
+        ref = tables_npz[name].astype(np.float32)
+        c = np.ascontiguousarray(ref[:, 1:, None])
+    else:
+        c = tables_npz[name].astype(np.float32)
+    want = orc.subdyadic_eval32(c, b, lattice_u)
+    for mode in (0, 1):
+        got, fast = lattice_eval(c, b, mode)
+        assert np.array_equal(bits(got), bits(want)), (name, mode)
+        if mode == 1:
+            assert fast == 1, "shipped table must take the signed-table fast path"
+
+
+@pytest.mark.parametrize("b", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("K", [3, 16, 23, 30])
+def test_random_tables_whole_lattice(arv, orc, lattice_u, b, K):
+    rng = np.random.default_rng(100 * K + b)
+    c = random_table(rng, K, b)
+    got, fast = lattice_eval(c, b, 1)
+    assert fast == 1
+    assert np.array_equal(bits(got), bits(orc.subdyadic_eval32(c, b, lattice_u)))
+
+
+def test_fallback_on_exact_zero(arv, orc, lattice_u):
+    """A linear piece with an exact zero at a lattice point: the reference gives
+    -0.0 on the upper half there, which the signed table cannot: the kernel
+    must detect it and run the general evaluator."""
+    rng = np.random.default_rng(7)
+    c = random_table(rng, 16, 3)
+    m = 3_500_001  # lattice point v = (m + 1/2) 2^-23 = 0.417 (octave 1)
+    v = np.float32((m + 0.5) * 2.0**-23)
+    c[1, 0, :] = 2.0
+    c[0, 0, :] = -np.float32(2.0) * v  # exact
+    want = orc.subdyadic_eval32(c, 3, lattice_u)
+    zero = want == 0
+    assert zero.any() and np.signbit(orc.subdyadic_eval32(c, 3, (np.float32(1) - lattice_u[zero]))).all()
+    got, fast = lattice_eval(c, 3, 1)
+    assert fast == 0
+    assert np.array_equal(bits(got), bits(want))
+    # the fused generator takes the same fallback: upper-half samples of that
+    # point come out as -0.0 like the reference
+    n = 1 << 22
+    out = arv.Pcg32Stream(11, 2).sample(_subtable(arv, c, 3), n)
+    assert np.array_equal(bits(out), bits(orc.pcg32_subdyadic_f32(11, 2, 0, c, 3, n)))
+
+
+def test_fallback_on_inexact_slope_scaling(arv, orc, lattice_u):
+    rng = np.random.default_rng(8)
+    c = random_table(rng, 12, 2)
+    c[1, 4, 1] = np.float32(3e-36)  # c1 * 2^-23 is subnormal and would round
+    got, fast = lattice_eval(c, 2, 1)
+    assert fast == 0
+    assert np.array_equal(bits(got), bits(orc.subdyadic_eval32(c, 2, lattice_u)))
+
+
+def _subtable(arv, c, b):
+    from paper_2012_09715_b200.tables import SubDyadicTable
+
+    return SubDyadicTable(degree=c.shape[0] - 1, n_octaves=c.shape[1], sub_bits=b, coeffs=c.astype(np.float64))
+
+
+@pytest.mark.parametrize("b", [0, 1, 2, 4, 5])
+def test_fused_generator_every_sub_bits(arv, orc, b):
+    """The fused generator at each sub_bits (b <= 4 signed table, b = 5 general)."""
+    rng = np.random.default_rng(b)
+    c = random_table(rng, 18, b)
+    n = (1 << 20) + 5
+    out = arv.Pcg32Stream(42, 0, counter=3).sample(_subtable(arv, c, b), n)
+    assert np.array_equal(bits(out), bits(orc.pcg32_subdyadic_f32(42, 0, 3, c, b, n)))
+
+
+def test_config2_full_output_sha256(arv, hashes):
+    """All 2^28 config-2 samples, bit for bit (the oracle's full-output hash)."""
+    out = arv.Pcg32Stream(42, 0).sample(arv.load_table("subdyadic_linear_k16_s8"), 1 << 28)
+    h = hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest()
+    assert h == hashes["config2_subdyadic_f32_sha256_2^28"]
+
+
+def test_pdl_table_written_by_previous_kernel(arv, orc, tables_npz):
+    """The generator is launched with programmatic dependent launch; its table
+    is staged after griddepcontrol.wait, so a table produced by the kernel
+    just before it on the stream is the one used (no stale read)."""
+    from paper_2012_09715_b200 import _device as dev
+    from paper_2012_09715_b200._native import call
+
+    base = tables_npz["subdyadic_linear_k16_s8"].astype(np.float32)
+    src = torch.from_numpy(base).cuda()
+    c = torch.zeros_like(src)
+    n = 1 << 22
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    s = dev.stream_handle()
+    for scale in (1.0, -1.0, 0.5, 2.0):
+        # a long-running kernel, then the table-writing kernel, then the generator
+        big = torch.empty(1 << 26, dtype=torch.float32, device="cuda")
+        call("arv_store_probe", big.data_ptr(), big.numel(), s)
+        torch.mul(src, scale, out=c)
+        call("arv_pcg32_subdyadic_f32", 42, 0, 0, c.data_ptr(), 1, 16, 3, out.data_ptr(), n, s)
+        ref = orc.pcg32_subdyadic_f32(42, 0, 0, (base * np.float32(scale)).astype(np.float32), 3, n)
+        assert np.array_equal(bits(out), bits(ref)), scale
