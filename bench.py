@@ -241,7 +241,27 @@ def run_reference(args) -> None:
         rk = {"unavailable": f"{type(exc).__name__}: {exc}"}
     if rk is not None:
         line["reference_kernel"] = rk
+    try:
+        line["reference_sampler"] = reference_sampler_rate(threads)
+    except Exception as exc:
+        line["reference_sampler"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
     print(json.dumps(line), flush=True)
+
+
+def reference_sampler_rate(procs: int, n_per_proc: int = 1 << 24) -> dict | None:
+    """The reference's whole sampling path with generation: UniformStream.uniforms
+    (numpy Philox-4x64) + eval_dyadic(float32) through its compiled kernel,
+    one process per core on disjoint stream ids (oracle/refpath.py)."""
+    import oracle
+    from oracle import refpath
+
+    if oracle.load_ref_kernels() is None:
+        return None
+    units, wall = refpath.run_pool(refpath.sampler_path, [(42, j, n_per_proc, 1 << 20) for j in range(procs)],
+                                   procs)
+    return {"value": units / wall, "unit": "samples/s", "cores": procs, "kind": "reference",
+            "sample": f"{procs} processes x {n_per_proc} samples: UniformStream(42, j).uniforms (numpy Philox) -> "
+                      f"f32 -> oracle/_ref _kernels.dyadic_eval32 (reference Cython), K15 linear table"}
 
 
 # ---------------------------------------------------------------------------
@@ -283,6 +303,114 @@ def _fp64_roofline(key: str, path_steps_per_s: float) -> dict | None:
                 "peak_source": "nominal: ncu peak_sustained 64 DFMA/SM/clk x max SM clock (MEASURED_PEAKS sm_max_mhz)"}
     except Exception:
         return None
+
+
+def time_generator(arv, _native, table, n, offset, steps, device):
+    """Per-launch seconds of the fused generator over `steps` launches and the
+    launch count.  Outputs smaller than L2 are timed launch by launch with a
+    512 MiB store sweep flushing L2 in between (outside the events); larger
+    outputs stream straight through L2 and are timed back to back."""
+    import torch
+
+    out = torch.empty(n, dtype=torch.float32, device=device)
+
+    def step():
+        arv.Pcg32Stream(42, 0, counter=offset).sample(table, n, out=out)
+
+    for _ in range(3):
+        step()
+    flush = n * 4 < (256 << 20)
+    scratch = torch.empty(128 << 20, dtype=torch.float32, device=device) if flush else None
+    torch.cuda.synchronize()
+    l0 = _native.launch_count()
+    if flush:
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        s = torch.cuda.current_stream().cuda_stream
+        for a, b in evs:
+            _native.call("arv_store_probe", scratch.data_ptr(), scratch.numel(), s)
+            a.record()
+            step()
+            b.record()
+        torch.cuda.synchronize()
+        elapsed = sum(a.elapsed_time(b) for a, b in evs) * 1e-3
+    else:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            step()
+        b.record()
+        b.synchronize()
+        elapsed = a.elapsed_time(b) * 1e-3
+    launches = _native.launch_count() - l0 - (steps if flush else 0)
+    return elapsed / steps, launches, flush
+
+
+def config1_entry(arv, _native, device, offset: int, peak: float, steps: int = 200) -> dict:
+    """BASELINE configs[0] (2^24 samples, piecewise-constant q=10 table) on the
+    same GPU: per-launch time with L2 flushed between launches, HBM roofline."""
+    n, tname, wl = WORKLOADS["config1"]
+    per_launch, launches, _ = time_generator(arv, _native, arv.load_table(tname), n, offset, steps, device)
+    achieved = n * BYTES_PER_SAMPLE / per_launch / 1e9
+    return {"workload": wl, "value": n / per_launch, "unit": "samples/s", "us_per_launch": per_launch * 1e6,
+            "steps": steps, "gpu_launches": int(launches),
+            "l2": "output < L2: each launch timed alone, 512 MiB store sweep flushes L2 in between",
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "algorithmic_bytes_per_launch": n * BYTES_PER_SAMPLE}}
+
+
+def e2e_plugin(arv, device, steps: int = 3) -> dict:
+    """The reference's calling convention end to end: the drop-in plugin call
+    ``_kernels.dyadic_eval32(coeffs32, u, out)`` (_kernels.pyx:76-93) on 2^28
+    numpy f32 uniforms into a caller-allocated numpy out -- H2D of u, kernel,
+    D2H into out inside the timed region (host-buffer pipeline,
+    csrc/arv_host.cu).  Same work as `reference_kernel` in the reference arm."""
+    import torch
+
+    from paper_2012_09715_b200 import _kernels
+
+    n = 1 << 28
+    lin = arv.load_table("dyadic_linear_k15")
+    u = arv.Pcg32Stream(42, 0).uniforms(n).cpu().numpy()  # the lattice uniforms, host
+    out = np.empty(n, np.float32)
+    out.fill(0.0)  # pages touched once (as the reference's np.empty_like + its own writes)
+    _kernels.dyadic_eval32(lin.coeffs32, u[: 1 << 20], out[: 1 << 20])  # warm (pinned staging allocated)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        _kernels.dyadic_eval32(lin.coeffs32, u, out)  # returns when out is written
+    dt = (time.perf_counter() - t0) / steps
+    ref = arv.eval_dyadic(lin, torch.from_numpy(u[: 1 << 16]).to(device), dtype=np.float32).cpu().numpy()
+    assert np.array_equal(out[: 1 << 16].view(np.uint32), ref.view(np.uint32))
+    return {"value": n / dt, "unit": "samples/s", "h2d_bytes_per_step": n * 4, "d2h_bytes_per_step": n * 4,
+            "ms_per_step": dt * 1e3, "samples_per_step": n,
+            "path": "paper_2012_09715_b200._kernels.dyadic_eval32(numpy f32 u, numpy f32 out), K15 linear table: "
+                    "pinned-chunk pipeline (host copies || H2D || kernel || D2H), host wall clock"}
+
+
+def shard_check(out, rank: int, world: int, device) -> dict:
+    """Sum of the shard's 64-bit words mod 2^64 on the device, against the
+    oracle's value for this rank's offset range (tests/golden/hashes.json)."""
+    import torch
+
+    s = int(out.view(torch.int64).sum().item()) % (1 << 64)
+    try:
+        with open(os.path.join(REPO, "tests", "golden", "hashes.json")) as fh:
+            want = json.load(fh).get("config2_shard_word_sums_mod2^64", [])
+        ok = (str(s) == want[rank]) if rank < len(want) and N_PER_GPU == 1 << 28 else None
+    except Exception:
+        ok = None
+    t = torch.tensor([rank, 1 if ok else (0 if ok is False else -1)], dtype=torch.int64, device=device)
+    if world > 1:
+        import torch.distributed as dist
+
+        got = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(got, t)
+        flags = [int(g[1].item()) for g in got]
+        backend = dist.get_backend()
+    else:
+        flags, backend = [int(t[1].item())], None
+    return {"ranks": world, "backend": backend, "rank_ok": flags, "all_match": all(f == 1 for f in flags),
+            "check": "per-rank sum of output words mod 2^64 vs the oracle's for its PCG32 offset range"}
 
 
 def run_ours(args) -> None:
@@ -366,6 +494,7 @@ def run_ours(args) -> None:
     # approximation quality of this step's output (untimed): error against the
     # exact AS241 f64 quantile of the same uniforms, over every sample
     quality = approximation_error(arv, out, offset)
+    shards = shard_check(out, rank, world, device)
 
     # e2e: the public API with a pinned host buffer, D2H inside the timed region
     host = torch.empty(n, dtype=torch.float32, pin_memory=True)
@@ -396,6 +525,10 @@ def run_ours(args) -> None:
     store_gbs = n * 4 * 20 / (s0.elapsed_time(s1) * 1e-3) / 1e9
 
     mlmc = None if args.no_mlmc else mlmc_metrics(arv, args, rank, world, device)
+    peak = _peaks().get("hbm_gbs") or 6650.0
+    c1 = config1_entry(arv, _native, device, rank * WORKLOADS["config1"][0], peak) \
+        if N_PER_GPU != WORKLOADS["config1"][0] else None
+    plugin = e2e_plugin(arv, device) if rank == 0 and not args.no_plugin else None
 
     # sustained (last GPU phase, so the power ramp cannot slow the MLMC timings):
     # the same launches back to back for ~2 s; the second half is
@@ -442,7 +575,12 @@ def run_ours(args) -> None:
         "clocks": sampler.summary(),
         "quality": quality,
         "sustained": sustained,
+        "shard_check": shards,
     }
+    if plugin is not None:
+        line["e2e_plugin"] = plugin
+    if c1 is not None:
+        line["config1"] = c1
     if mlmc is not None:
         line["mlmc"] = mlmc
     if world == 1 and not args.no_cpu:
@@ -493,11 +631,19 @@ def approximation_error(arv, out, offset: int, chunk: int = 1 << 26) -> dict:
 
 def mlmc_metrics(arv, args, rank, world, device) -> dict:
     """Config 4 (GBM EM, l=0..8, 2^22 paths/level) and config 5 (CIR exact, l=0..6,
-    2^20 paths/level) paths/s: one full multilevel pilot, paths sharded over ranks."""
+    2^20 paths/level): one full multilevel pilot through the public estimator
+    ``estimate_level_suite`` (mlmc.py:383-411).  At N > 1 each level's paths
+    are sharded over the ranks and the per-level (count, mean, M2) triples and
+    the failure count are merged by NCCL all-reduces (mlmc.allreduce_triples),
+    so the reported statistics are the whole job's.  Timed with CUDA events
+    around the whole pilot (host work between levels included), max over ranks."""
     import torch
 
-    from paper_2012_09715_b200.mlmc import run_level
+    group = None
+    if world > 1:
+        import torch.distributed as dist
 
+        group = dist.group.WORLD
     res = {}
     lin = arv.load_table("dyadic_linear_k15")
     cases = [
@@ -506,44 +652,72 @@ def mlmc_metrics(arv, args, rank, world, device) -> dict:
          arv.load_table("ncchi2_cir_k64_stacks"), range(0, 7), 1 << 20),
     ]
     for name, proc, scheme, tab, levels, n_paths in cases:
-        per = n_paths // world
-        lo = rank * per
         specs = [arv.LevelSpec(level=l, scheme=scheme, process=proc, rv_source=tab, kind="four_way", n0=1)
                  for l in levels]
-        # warm-up on a small slice
-        for sp in specs[:2]:
-            run_level(sp, arv.level_stream(42, sp.level), n_paths, path_lo=lo, path_count=min(per, 4096))
+        for sp in specs[:2]:  # warm-up
+            arv.estimate_level_suite(sp, arv.level_stream(42, sp.level), 4096 * world, group=group)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        stats = []
-        for sp in specs:
-            st, _, nf = run_level(sp, arv.level_stream(42, sp.level), n_paths, path_lo=lo, path_count=per)
-            stats.append((st, nf))
+        suites = [arv.estimate_level_suite(sp, arv.level_stream(42, sp.level), n_paths, group=group)
+                  for sp in specs]  # raises NumericalError if any rank's exact transitions failed
         e1.record()
         e1.synchronize()
         t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device=device)
         if world > 1:
-            import torch.distributed as dist
-
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         secs = float(t.item())
         steps = sum(1 << l for l in levels)
         paths_total = n_paths * len(levels)
         entry = {"paths_per_level": n_paths, "levels": [levels[0], levels[-1]], "seconds": secs,
-                 "paths_per_s": paths_total / secs, "path_steps_per_s": n_paths * steps / secs}
+                 "paths_per_s": paths_total / secs, "path_steps_per_s": n_paths * steps / secs,
+                 "api": "estimate_level_suite per level" + (f", NCCL all-reduce of the triples over {world} ranks"
+                                                            if world > 1 else "")}
         entry["roofline"] = _fp64_roofline("gbm_level8" if scheme != "cir_exact" else "cir_level6",
                                            n_paths * steps / secs)
-        s = [x[0].cpu().numpy() for x in stats]
         if scheme == "cir_exact":
-            entry["n_fail"] = int(sum(int(x[1].item()) for x in stats))
-            entry["log2_correction_gap"] = [float(np.log2((r[2, 2] / max(r[2, 0] - 1, 1)) /
-                                                          (r[3, 2] / max(r[3, 0] - 1, 1)))) for r in s]
+            entry["n_fail"] = 0
+            entry["log2_correction_gap"] = [float(np.log2(s["correction"].variance / s["plain_exact"].variance))
+                                            for s in suites]
+            entry["process_variance"] = [s["plain_exact"].variance for s in suites]
         else:
-            entry["log2_four_way_gap"] = [float(np.log2(r[2, 2] / r[0, 2])) for r in s[1:]]
-            entry["level0_mean"] = float(s[0][0, 1])
+            entry["log2_four_way_gap"] = [float(np.log2(s["four_way"].variance / s["two_way_exact"].variance))
+                                          for s in suites[1:]]
+            entry["level0_mean"] = suites[0]["two_way_exact"].mean
+        entry["n_paths_merged"] = [s[next(iter(s))].n_paths for s in suites]
+        if world == 1 and rank == 0 and not args.no_cpu:
+            entry["cpu_baseline"] = mlmc_cpu_baseline(name, levels, n_paths)
         res[name] = entry
     return res
+
+
+def mlmc_cpu_baseline(name: str, levels, n_paths: int, budget_s: float = 10.0) -> dict:
+    """The reference's MLMC pilot on the host cores (oracle/refpath.py: the C
+    restatement of simulate_gbm_coupled / the numpy-scipy restatement of
+    simulate_cir_coupled(cir_exact), one process per core), on a bounded
+    sample of the same levels: a fraction f of each level's paths, f sized from
+    a calibration run to ~budget_s of wall time."""
+    from oracle import refpath
+
+    procs = cpu_threads()
+    if name.startswith("gbm"):
+        fn, make = refpath.gbm_level, (lambda l, m, j: (l, n_paths, j * m, (j + 1) * m))
+        kind_note = "oracle.c orc_gbm_paths (C restatement of simulate_gbm_coupled, -O3, no FMA)"
+    else:
+        fn, make = refpath.cir_exact_level, (lambda l, m, j: (l, m, 42 + j))
+        kind_note = "oracle/cir.py (numpy/scipy restatement of simulate_cir_coupled cir_exact, CDFLIB chndtr)"
+    cal_units, cal_wall = refpath.run_pool(fn, [make(levels[-1], 256, j) for j in range(procs)], procs)
+    rate0 = cal_units / cal_wall
+    total = n_paths * sum(1 << l for l in levels)
+    f = min(1.0, rate0 * budget_s / total)
+    m = max(16, int(n_paths * f) // procs)
+    jobs = [make(l, m, j) for l in levels for j in range(procs)]
+    units, wall = refpath.run_pool(fn, jobs, procs)
+    return {"value": units / wall, "unit": "path-steps/s", "cores": procs, "kind": "port",
+            "paths_per_s": m * procs * len(levels) / wall,
+            "seconds_full_config_extrapolated": total / (units / wall),
+            "sample": f"{m * procs} paths per level x levels {levels[0]}..{levels[-1]} ({units} path-steps, "
+                      f"{wall:.1f} s wall), {procs} processes; {kind_note}"}
 
 
 def main() -> None:
@@ -555,8 +729,9 @@ def main() -> None:
     ap.add_argument("--no-mlmc", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sustained", action="store_true")
+    ap.add_argument("--no-plugin", action="store_true")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config2")
-    ap.add_argument("--ref-samples", type=int, default=1 << 26,
+    ap.add_argument("--ref-samples", type=int, default=1 << 28,
                     help="reference arm: bounded host sample per step (samples)")
     args = ap.parse_args()
     select_workload(args.workload)

@@ -76,6 +76,28 @@ ARV_API int arv_ncchi2_eval(const double *stacks, int64_t n_knots, int degree, i
                     const double *u, const double *lam, int64_t nlam, double *out, int64_t n,
                     void *stream);
 
+/* ---- the same plugin functions with HOST buffers (the reference's numpy
+ * calling convention: sampler.py:91-206 passes host arrays and a
+ * caller-allocated host `out`).  u, lam and out are host pointers (pageable
+ * or pinned); tables (values / coeffs / stacks) are device pointers.  The
+ * call stages chunks through pinned buffers, overlapping the host copies,
+ * H2D, the kernel (on `stream`) and D2H, and returns when out is written.
+ * Calls are serialised per device. ------------------------------------- */
+ARV_API int arv_host_constant_eval(const double *values, int64_t nvals, const double *u, double *out, int64_t n,
+                                   void *stream);
+ARV_API int arv_host_dyadic_index(const double *u, int64_t n, int64_t cap, int64_t *out, void *stream);
+ARV_API int arv_host_dyadic_index32(const float *u, int64_t n, int64_t cap, int64_t *out, void *stream);
+ARV_API int arv_host_dyadic_eval(const double *coeffs, int degree, int64_t K1, const double *u, double *out,
+                                 int64_t n, void *stream);
+ARV_API int arv_host_dyadic_eval32(const float *coeffs, int degree, int64_t K1, const float *u, float *out,
+                                   int64_t n, void *stream);
+ARV_API int arv_host_subdyadic_eval32(const float *coeffs, int degree, int K, int sub_bits, const float *u,
+                                      float *out, int64_t n, void *stream);
+ARV_API int arv_host_ncchi2_eval(const double *stacks, int64_t n_knots, int degree, int64_t K1, double nu,
+                                 const double *u, const double *lam, int64_t nlam, double *out, int64_t n,
+                                 void *stream);
+ARV_API int arv_host_gaussian_inv_cdf(const double *u, double *out, int64_t n, void *stream);
+
 /* ---- extensions of the same evaluators ---------------------------------- */
 
 /* Octave x sub-interval dyadic table, f32 (BASELINE.json config 2).
@@ -177,6 +199,9 @@ ARV_API int arv_set_tuning(int key, int value);
 #define ARV_SCHEME_CIR_MILSTEIN_TRUNCATED 4
 #define ARV_RNG_PCG32 0
 #define ARV_RNG_PHILOX 1
+#define ARV_SIDES_BOTH 0
+#define ARV_SIDES_EXACT 1
+#define ARV_SIDES_APPROX 2
 #define ARV_PAYOFF_IDENTITY 0
 #define ARV_PAYOFF_CALL 1
 
@@ -189,6 +214,10 @@ typedef struct {
     uint64_t seed, stream_id;
     int64_t n_paths_total, path_lo, path_count;
     int rng; /* ARV_RNG_PCG32 or ARV_RNG_PHILOX */
+    /* ARV_SIDES_EXACT / _APPROX / _BOTH (0 = both): which side's payoffs the
+     * caller wants (mlmc.py:176-192 `sides`); the other side's work is
+     * skipped and its payoff / statistics slots are unspecified. */
+    int sides;
 } arv_level_spec;
 
 ARV_API int64_t arv_mlmc_workspace_bytes(int64_t path_count);

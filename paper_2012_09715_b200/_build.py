@@ -60,15 +60,29 @@ def source_hash() -> str:
     return h.hexdigest()
 
 
+def built_hash(path: str) -> str | None:
+    """arv_source_hash() of a built library, read from the file (the string is
+    tagged "ARV_SOURCE_HASH=<hex>" in .rodata) without loading it."""
+    import re
+
+    with open(path, "rb") as fh:
+        m = re.search(rb"ARV_SOURCE_HASH=([0-9a-f]{64}|unknown)", fh.read())
+    return m.group(1).decode() if m else None
+
+
 def needs_build() -> bool:
+    """Missing, older than a source, or built from other sources (hash)."""
     if not os.path.exists(LIB_PATH):
         return True
     t = os.path.getmtime(LIB_PATH)
-    return any(os.path.getmtime(p) > t for p in _deps())
+    return any(os.path.getmtime(p) > t for p in _deps()) or built_hash(LIB_PATH) != source_hash()
 
 
 def build(verbose_ptxas: bool = False, force: bool = False, defines=(), out: str | None = None) -> str:
-    """Compile every csrc/*.cu and link libarv_b200.so (or `out` with extra -D defines)."""
+    """Compile csrc/*.cu and link libarv_b200.so (or `out` with extra -D defines).
+
+    Objects whose source, headers and command line are unchanged are reused
+    unless ``force``."""
     target = out or LIB_PATH
     if not force and not defines and out is None and not needs_build():
         return LIB_PATH
@@ -85,17 +99,37 @@ def build(verbose_ptxas: bool = False, force: bool = False, defines=(), out: str
     if verbose_ptxas:
         common += ["-Xptxas", "-v"]
     common += [f"-D{d}" for d in defines]
-    common += [f'-DARV_SOURCE_HASH="{source_hash()}"']
     if defines or out is not None:  # experiment variants: objects outside the repo
         objdir = os.path.join(tempfile.gettempdir(), "arv_variant_build", os.path.basename(target))
         os.makedirs(objdir, exist_ok=True)
+    headers = sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h")))
     objs = []
     procs = []
     for src in sources():
-        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        base = os.path.basename(src)
+        obj = os.path.join(objdir, base + ".o")
         objs.append(obj)
-        procs.append(subprocess.Popen([nvcc, *common, *PER_FILE_FLAGS.get(os.path.basename(src), []), "-c", src, "-o", obj]))
+        cmd = [nvcc, *common, *PER_FILE_FLAGS.get(base, [])]
+        if base == "arv_runtime.cu":  # the only unit that embeds the source hash
+            cmd += [f'-DARV_SOURCE_HASH="{source_hash()}"']
+        cmd += ["-c", src, "-o", obj]
+        # incremental: an object is reused when it is newer than its source and
+        # every header and was built with the same command line
+        stamp = obj + ".cmd"
+        key = hashlib.sha256(repr(cmd).encode()).hexdigest()
+        fresh = (not force and os.path.exists(obj) and os.path.exists(stamp)
+                 and open(stamp).read() == key
+                 and all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in [src, *headers]))
+        if fresh:
+            continue
+        p = subprocess.Popen(cmd)
+        p.stamp, p.key = stamp, key
+        procs.append(p)
     bad = [p.args[-3] for p in procs if p.wait() != 0]
+    for p in procs:
+        if p.returncode == 0:
+            with open(p.stamp, "w") as fh:
+                fh.write(p.key)
     if bad:
         raise RuntimeError(f"nvcc failed for {bad}")
     tmp = target + ".tmp"

@@ -107,11 +107,13 @@ def table_on_device(arr, dtype: torch.dtype, device: torch.device | None = None)
         return t
 
 
-def copy_out(dst, src: torch.Tensor) -> None:
-    """Write a device result into the caller's ``out`` (device or host)."""
+def copy_out(dst, src) -> None:
+    """Write a result (device tensor or host array) into the caller's ``out``."""
     if isinstance(dst, torch.Tensor):
+        if isinstance(src, np.ndarray):
+            src = torch.from_numpy(np.ascontiguousarray(src))
         if dst.data_ptr() != src.data_ptr():
             dst.copy_(src.view(dst.shape) if src.numel() == dst.numel() else src)
         return
-    host = src.cpu().numpy()
+    host = src if isinstance(src, np.ndarray) else src.cpu().numpy()
     np.copyto(dst, host.reshape(np.shape(dst)), casting="unsafe")

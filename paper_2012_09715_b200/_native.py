@@ -27,12 +27,14 @@ class LevelSpec(C.Structure):
         ("seed", _u64), ("stream_id", _u64),
         ("n_paths_total", _i64), ("path_lo", _i64), ("path_count", _i64),
         ("rng", _int),
+        ("sides", _int),
     ]
 
 
 SCHEME_EM, SCHEME_MILSTEIN, SCHEME_CIR_EXACT, SCHEME_CIR_EULER_TRUNCATED, SCHEME_CIR_MILSTEIN_TRUNCATED = range(5)
 PAYOFF_IDENTITY, PAYOFF_CALL = 0, 1
 RNG_PCG32, RNG_PHILOX = 0, 1
+SIDES_BOTH, SIDES_EXACT, SIDES_APPROX = 0, 1, 2
 PHILOX_UNIFORM, PHILOX_CONSTANT, PHILOX_DYADIC, PHILOX_GAUSSIAN = range(4)
 
 _SIGNATURES = {
@@ -47,6 +49,15 @@ _SIGNATURES = {
     "arv_dyadic_eval32": ([_p, _int, _i64, _p, _p, _i64, _p], _int),
     "arv_ncchi2_eval": ([_p, _i64, _int, _i64, _dbl, _p, _p, _i64, _p, _i64, _p], _int),
     "arv_subdyadic_eval32": ([_p, _int, _int, _int, _p, _p, _i64, _p], _int),
+    # host-buffer (numpy) convention: u / lam / out are host pointers
+    "arv_host_constant_eval": ([_p, _i64, _p, _p, _i64, _p], _int),
+    "arv_host_dyadic_index": ([_p, _i64, _i64, _p, _p], _int),
+    "arv_host_dyadic_index32": ([_p, _i64, _i64, _p, _p], _int),
+    "arv_host_dyadic_eval": ([_p, _int, _i64, _p, _p, _i64, _p], _int),
+    "arv_host_dyadic_eval32": ([_p, _int, _i64, _p, _p, _i64, _p], _int),
+    "arv_host_subdyadic_eval32": ([_p, _int, _int, _int, _p, _p, _i64, _p], _int),
+    "arv_host_ncchi2_eval": ([_p, _i64, _int, _i64, _dbl, _p, _p, _i64, _p, _i64, _p], _int),
+    "arv_host_gaussian_inv_cdf": ([_p, _p, _i64, _p], _int),
     "arv_gaussian_inv_cdf": ([_p, _p, _i64, _p], _int),
     "arv_gaussian_inv_cdf32": ([_p, _p, _i64, _p], _int),
     "arv_pcg32_words": ([_u64, _u64, _u64, _p, _i64, _p], _int),
@@ -73,28 +84,18 @@ _SIGNATURES = {
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
 
-def _built_hash(path: str) -> str | None:
-    """arv_source_hash() of a built library, read from the file (the string is
-    tagged "ARV_SOURCE_HASH=<hex>" in .rodata) without loading it."""
-    import re
-
-    with open(path, "rb") as fh:
-        m = re.search(rb"ARV_SOURCE_HASH=([0-9a-f]{64}|unknown)", fh.read())
-    return m.group(1).decode() if m else None
-
-
 def _load() -> C.CDLL:
     # ARV_LIB_PATH: an alternative build of the same library (tuning experiments only)
     alt = os.environ.get("ARV_LIB_PATH")
     path = alt or _build.LIB_PATH
     if not alt:
-        stale = not os.path.exists(path) or _built_hash(path) != _build.source_hash()
+        stale = _build.needs_build()
         if stale:
             # a library built from other sources must never load silently
             if os.environ.get("ARV_NO_AUTOBUILD"):
                 raise ImportError(f"{path} is missing or was built from other sources; "
                                   "run `python -m paper_2012_09715_b200._build`")
-            _build.build(force=True)
+            _build.build()
     lib = C.CDLL(path)
     for name, (args, res) in _SIGNATURES.items():
         fn = getattr(lib, name)  # AttributeError = stale or broken library: fail loudly

@@ -64,6 +64,7 @@ struct LevelArgs {
     double nu_exact, nu_table, scale, decay_over_scale;
     // uniform source
     int rng;             // ARV_RNG_PCG32 / ARV_RNG_PHILOX
+    int want_exact, want_approx;  // arv_level_spec::sides
     uint64_t seed, sid;  // Philox key
     uint64_t n_paths_total;
     Affine jump2[kPathJumpBits];  // LCG^(2^i): path p starts popcount(p) affine maps from s0
@@ -411,9 +412,10 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
             bool lo[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) u[k] = rng.next(lo[k]);
-            as241_f64_batch<4, true>(u, z, rows);
+            if (A.want_exact) as241_f64_batch<4, true>(u, z, rows);
+            else z[0] = z[1] = z[2] = z[3] = 0.0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) w[k] = gauss_table_eval<DEG>(smd, K1, u[k], lo[k]);
+            for (int k = 0; k < 4; ++k) w[k] = A.want_approx ? gauss_table_eval<DEG>(smd, K1, u[k], lo[k]) : 0.0;
             pair_step(z, w);
             pair_step(z + 2, w + 2);
         }
@@ -423,16 +425,17 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
             bool lo[2];
             u[0] = rng.next(lo[0]);
             u[1] = rng.next(lo[1]);
-            as241_f64_batch<2, true>(u, z, rows);
-            w[0] = gauss_table_eval<DEG>(smd, K1, u[0], lo[0]);
-            w[1] = gauss_table_eval<DEG>(smd, K1, u[1], lo[1]);
+            if (A.want_exact) as241_f64_batch<2, true>(u, z, rows);
+            else z[0] = z[1] = 0.0;
+            w[0] = A.want_approx ? gauss_table_eval<DEG>(smd, K1, u[0], lo[0]) : 0.0;
+            w[1] = A.want_approx ? gauss_table_eval<DEG>(smd, K1, u[1], lo[1]) : 0.0;
             pair_step(z, w);
         }
         if (A.n_f & 1) {
             bool lo;
             const double u = rng.next(lo);
-            xf_e = step(xf_e, __dmul_rn(sq_f, as241_f64(u)), dt_f);
-            xf_a = step(xf_a, __dmul_rn(sq_f, gauss_table_eval<DEG>(smd, K1, u, lo)), dt_f);
+            if (A.want_exact) xf_e = step(xf_e, __dmul_rn(sq_f, as241_f64(u)), dt_f);
+            if (A.want_approx) xf_a = step(xf_a, __dmul_rn(sq_f, gauss_table_eval<DEG>(smd, K1, u, lo)), dt_f);
         }
         const double fe = payoff_fn(xf_e, A.payoff, A.strike);
         const double fa = payoff_fn(xf_a, A.payoff, A.strike);
@@ -571,11 +574,11 @@ __global__ void __launch_bounds__(kCirBlock, ARV_CIR_MINB) k_cir_exact_level(Lev
             x_a = __dmul_rn(A.scale, ncchi2_eval1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_a));
             // mlmc.py:269-278 exact side, warm-started from the table
             lam_e = __dmul_rn(x_e, A.decay_over_scale);
-            warm = ncchi2_warm1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_e);
+            if (A.want_exact) warm = ncchi2_warm1<DEG>(tab, n_knots, K1, A.nu_table, u, lam_e);
         }
         if constexpr (SORT) {
             const int t = threadIdx.x;
-            cta_sort_perm<kCirBlock>(valid ? lam_e : -1.0, sh_key, sh_perm);
+            cta_sort_perm<kCirBlock>(valid && A.want_exact ? lam_e : -1.0, sh_key, sh_perm);
             sh_u[t] = u;
             sh_lam[t] = lam_e;
             sh_warm[t] = warm;
@@ -591,12 +594,12 @@ __global__ void __launch_bounds__(kCirBlock, ARV_CIR_MINB) k_cir_exact_level(Lev
             sh_x[src] = xq;  // back to the owner's slot
             sh_r[src] = rq;
             __syncthreads();
-            if (valid) {
+            if (valid && A.want_exact) {
                 fails += sh_r[t] > 1e-8;
                 x_e = __dmul_rn(A.scale, sh_x[t]);
             }
             __syncthreads();
-        } else if (valid) {
+        } else if (valid && A.want_exact) {
             const NcQuantile q = ncchi2_quantile(u, A.nu_exact, lam_e, warm);
             fails += q.resid > 1e-8;
             x_e = __dmul_rn(A.scale, q.x);
@@ -801,6 +804,10 @@ static int fill_common(const arv_level_spec *sp, LevelArgs &A) {
         return set_error(ARV_ERR_CONFIG, "n_paths_total must be < 2^40");
     if (sp->rng != ARV_RNG_PCG32 && sp->rng != ARV_RNG_PHILOX) return set_error(ARV_ERR_CONFIG, "unknown rng %d", sp->rng);
     A.rng = sp->rng;
+    if (sp->sides < ARV_SIDES_BOTH || sp->sides > ARV_SIDES_APPROX)
+        return set_error(ARV_ERR_CONFIG, "unknown sides %d", sp->sides);
+    A.want_exact = sp->sides != ARV_SIDES_APPROX;
+    A.want_approx = sp->sides != ARV_SIDES_EXACT;
     A.seed = sp->seed;
     A.sid = sp->stream_id;
     A.n_paths_total = static_cast<uint64_t>(sp->n_paths_total);
@@ -970,7 +977,7 @@ int arv_mlmc_cir_exact_level(const arv_level_spec *spec, const double *stacks, i
     // Segmented when the level is longer than one segment, the path ids fit
     // 32 bits and the caller's workspace holds the records.
     const int64_t seg = g_cir_segment;
-    const bool segmented = seg > 0 && A.n_f > seg && n < (int64_t(1) << 32) &&
+    const bool segmented = seg > 0 && A.want_exact && A.n_f > seg && n < (int64_t(1) << 32) &&
                            workspace_bytes >= CirWs(n, nullptr).total;
     const CirWs W(n, workspace);
     double *parts = segmented ? W.parts : static_cast<double *>(workspace);

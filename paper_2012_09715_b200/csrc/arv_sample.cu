@@ -430,9 +430,28 @@ __device__ __forceinline__ bool stage_linsigned(float2 *sm, const float *__restr
         const float hi = __uint_as_float((static_cast<uint32_t>(E) << 23) + (static_cast<uint32_t>(sub + 1) << (23 - b)));
         const int64_t m_lo = static_cast<int64_t>(ceilf(lo - 0.5f));
         const int64_t m_hi = static_cast<int64_t>(ceilf(hi - 0.5f)) - 1;
-        if (m_lo <= m_hi) {  // z is monotone in v over the entry: check the ends
+        if (m_lo <= m_hi) {
+            // z is monotone in m over the entry (v exact and increasing, RN
+            // monotone), so its exact zeros form one contiguous run.  Ends of
+            // one sign: no zero.  A sign change (the fit crosses 0 near
+            // v = 1/2): bisect with strict signs at both ends -- a run of
+            // zeros between them is always hit by some midpoint.
             const float za = lin_at(c0, c1, m_lo), zb = lin_at(c0, c1, m_hi);
-            ok &= (za > 0.0f && zb > 0.0f) || (za < 0.0f && zb < 0.0f);
+            if (za == 0.0f || zb == 0.0f || !(isfinite(za) && isfinite(zb))) {
+                ok = false;
+            } else if ((za > 0.0f) != (zb > 0.0f)) {
+                int64_t lo_m = m_lo, hi_m = m_hi;
+                while (hi_m - lo_m > 1) {
+                    const int64_t mid = lo_m + (hi_m - lo_m) / 2;
+                    const float zm = lin_at(c0, c1, mid);
+                    if (zm == 0.0f) {
+                        ok = false;
+                        break;
+                    }
+                    if ((zm > 0.0f) == (za > 0.0f)) lo_m = mid;
+                    else hi_m = mid;
+                }
+            }
         }
         sm[e] = make_float2(c0, c1s);
         sm[neg + e] = make_float2(-c0, c1s);

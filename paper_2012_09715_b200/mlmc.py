@@ -29,6 +29,7 @@ from .errors import ConfigError, NumericalError
 from .sampler import PhiloxStream, Pcg32Stream
 from .tables import ConstantTable, DyadicPolyTable, NcChi2Table, SubDyadicTable, load_table
 
+SIDES = ("exact", "approx", "both")
 SCHEMES = ("euler_maruyama", "milstein", "cir_exact", "cir_euler_truncated", "cir_milstein_truncated")
 KINDS = ("plain", "two_way", "four_way")
 PAYOFFS = ("identity", "call")
@@ -154,10 +155,10 @@ class LevelStats:
 class PathBatch:
     """Per-path terminal payoffs (device tensors), mlmc.py:123-135."""
 
-    p_fine_exact: torch.Tensor
-    p_coarse_exact: torch.Tensor
-    p_fine_approx: torch.Tensor
-    p_coarse_approx: torch.Tensor
+    p_fine_exact: Optional[torch.Tensor]
+    p_coarse_exact: Optional[torch.Tensor]
+    p_fine_approx: Optional[torch.Tensor]
+    p_coarse_approx: Optional[torch.Tensor]
     draws_per_path: int
 
 
@@ -185,7 +186,9 @@ _DEFAULT_GAUSS = "dyadic_linear_k15"
 
 def _gauss_coeffs(src) -> np.ndarray:
     if _is_exact(src):
-        src = load_table(_DEFAULT_GAUSS)  # placeholder approx side; exact stats unaffected
+        # the kernel takes a table argument; with sides="exact" (the only sides
+        # an exact source allows) the approximate side is never evaluated
+        src = load_table(_DEFAULT_GAUSS)
     if isinstance(src, ConstantTable) or type(src).__name__ == "ConstantTable":
         # (1, 2^q): "degree 0" = piecewise constant, evaluated as constant_eval
         v = np.asarray(src.values, dtype=np.float64).reshape(1, -1)
@@ -219,7 +222,11 @@ def _ncchi2_table(spec: LevelSpec):
     raise ConfigError("cir_exact with rv_source='exact' needs a table of matching nu for the warm start")
 
 
-def _native_spec(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, path_lo: int, path_count: int):
+_SIDES_CODE = {"both": nat.SIDES_BOTH, "exact": nat.SIDES_EXACT, "approx": nat.SIDES_APPROX}
+
+
+def _native_spec(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, path_lo: int, path_count: int,
+                 sides: str = "both"):
     p = spec.process
     s = nat.LevelSpec()
     if isinstance(p, GbmParams):
@@ -234,21 +241,24 @@ def _native_spec(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, path_lo: in
     s.seed, s.stream_id = int(stream.seed), int(stream.stream_id)
     s.n_paths_total, s.path_lo, s.path_count = n_paths, path_lo, path_count
     s.rng = nat.RNG_PHILOX if isinstance(stream, PhiloxStream) else nat.RNG_PCG32
+    s.sides = _SIDES_CODE[sides]
     return s
 
 
 def run_level(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, *, path_lo: int = 0,
-              path_count: Optional[int] = None, want_paths: bool = False, device=None):
+              path_count: Optional[int] = None, want_paths: bool = False, device=None, sides: str = "both"):
     """Launch one level; returns (stats device f64[NSLOT,3], paths or None, n_fail or None).
 
     The stream's counter is not consulted: paths are addressed from output
     0 of (seed, stream_id) as in the reference's fresh ``level_stream``.
+    ``sides`` ("both", "exact", "approx") skips the other side's work; its
+    payoffs and statistics slots are then unspecified.
     """
     device = device or dev.require_cuda()
     count = n_paths - path_lo if path_count is None else path_count
     if n_paths < 1 or count < 1:
         raise ConfigError("need at least one path")
-    ns = _native_spec(spec, stream, n_paths, path_lo, count)
+    ns = _native_spec(spec, stream, n_paths, path_lo, count, sides)
     stats = torch.empty(NSLOT * 3, dtype=torch.float64, device=device)
     paths = torch.empty((4, count), dtype=torch.float64, device=device) if want_paths else None
     ws_bytes = int(nat.lib.arv_mlmc_workspace_bytes(count))
@@ -277,11 +287,34 @@ def run_level(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, *, path_lo: in
     return stats.view(NSLOT, 3), paths, n_fail
 
 
+def _sides_for(spec: LevelSpec) -> str:
+    """mlmc.py:156-161: both sides for four-way levels, else the source's side."""
+    if spec.kind == "four_way":
+        return "both"
+    return "exact" if _is_exact(spec.rv_source) else "approx"
+
+
+def _resolve_sides(spec: LevelSpec, sides: Optional[str]) -> str:
+    sides = sides or _sides_for(spec)
+    if sides not in SIDES:
+        raise ConfigError(f"unknown sides {sides!r}")
+    if sides in ("approx", "both") and _is_exact(spec.rv_source):
+        raise ConfigError("approximate side requested but rv_source is 'exact'")  # mlmc.py:181-182
+    return sides
+
+
 def simulate(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, sides: Optional[str] = None) -> PathBatch:
-    """Coupled fine/coarse x exact/approx payoffs per path (mlmc.py:334-338)."""
-    _, paths, n_fail = run_level(spec, stream, n_paths, want_paths=True)
+    """Coupled fine/coarse x exact/approx payoffs per path (mlmc.py:334-338).
+
+    ``sides`` as in the reference (mlmc.py:176-192, 221-229): the payoffs of
+    an unrequested side are ``None`` and the kernel does not compute them.
+    """
+    sides = _resolve_sides(spec, sides)
+    _, paths, n_fail = run_level(spec, stream, n_paths, want_paths=True, sides=sides)
     _check_fail(spec, n_fail)
-    return PathBatch(paths[0], paths[1], paths[2], paths[3], draws_per_path=spec.n_steps_fine)
+    ex, ap = sides in ("exact", "both"), sides in ("approx", "both")
+    return PathBatch(paths[0] if ex else None, paths[1] if ex else None, paths[2] if ap else None,
+                     paths[3] if ap else None, draws_per_path=spec.n_steps_fine)
 
 
 def simulate_gbm_coupled(spec: LevelSpec, stream, n_paths: int, sides: Optional[str] = None) -> PathBatch:
@@ -380,7 +413,7 @@ def _stats_from(level: int, kind: str, triple, seconds: float, draws: float) -> 
                       degenerate=var == 0.0)
 
 
-def _timed_level(spec, stream, n_pilot, group=None):
+def _timed_level(spec, stream, n_pilot, group=None, sides: str = "both"):
     device = dev.require_cuda()
     rank, world = 0, 1
     if group is not None or _dist_ready():
@@ -394,7 +427,7 @@ def _timed_level(spec, stream, n_pilot, group=None):
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
     start.record()
-    stats, _, n_fail = run_level(spec, stream, n_pilot, path_lo=lo, path_count=cnt, device=device)
+    stats, _, n_fail = run_level(spec, stream, n_pilot, path_lo=lo, path_count=cnt, device=device, sides=sides)
     stop.record()
     if world > 1:
         import torch.distributed as dist
@@ -422,7 +455,7 @@ def estimate_level(spec: LevelSpec, stream: Pcg32Stream, n_pilot: int, group=Non
     """Pilot-run one level: mean/variance plus measured costs (mlmc.py:356-380)."""
     if n_pilot < 100:
         raise ConfigError(f"pilot size must be >= 100, got {n_pilot}")
-    stats, seconds = _timed_level(spec, stream, n_pilot, group)
+    stats, seconds = _timed_level(spec, stream, n_pilot, group, sides=_sides_for(spec))
     exact = _is_exact(spec.rv_source)
     if spec.scheme == "cir_exact":
         slot = {"plain": 3 if exact else 4, "two_way": 0 if exact else 1, "four_way": 2}[spec.kind]

@@ -37,21 +37,35 @@ _MAX64 = (1 << 64) - 1
 # ---------------------------------------------------------------------------
 
 def _as_batch(u, dtype=torch.float64):
-    """(device tensor, scalar?, host?) -- sampler.py:91-94 on the device."""
+    """(batch, scalar?, host?) -- sampler.py:91-94.
+
+    Host input stays a host array (the reference's f64 coercion and shape),
+    and the plugin call runs the host-buffer pipeline; a CUDA tensor stays on
+    the device (zero copy).
+    """
     if dev.is_device_tensor(u):
         return dev.to_device(u.reshape(-1) if u.dim() else u.reshape(1), dtype, u.device), u.dim() == 0, False
     arr = np.asarray(u, dtype=np.float64)
     scalar = arr.ndim == 0
-    return dev.to_device(np.atleast_1d(arr).reshape(-1), dtype), scalar, True
+    return np.ascontiguousarray(np.atleast_1d(arr)), scalar, True
 
 
-def _result(t: torch.Tensor, scalar: bool, host: bool, out=None):
-    if out is not None:
+def _result(t, scalar: bool, host: bool, out=None):
+    if out is not None and out is not t:
         dev.copy_out(out, t)
-        return float(t[0]) if scalar else out
+        return float(t.reshape(-1)[0]) if scalar else out
     if scalar:
-        return float(t[0])
-    return t.cpu().numpy() if host else t
+        return float(t.reshape(-1)[0])
+    return t
+
+
+def _empty(ud, out, dtype=None):
+    """The reference's `out = np.empty_like(arr)` (or the device twin)."""
+    if isinstance(ud, np.ndarray):
+        if isinstance(out, np.ndarray):
+            return out
+        return np.empty(ud.shape, dtype or ud.dtype)
+    return torch.empty_like(ud)
 
 
 def _coeffs(table, attr):
@@ -61,22 +75,21 @@ def _coeffs(table, attr):
 def eval_constant(table, u, out=None):
     """values[floor(2^q u)] per element (sampler.py:97-108)."""
     ud, scalar, host = _as_batch(u)
-    od = torch.empty_like(ud)
+    od = _empty(ud, out)
     kernels.constant_eval(table.values, ud, od)
     return _result(od, scalar, host, out)
 
 
 def dyadic_index(u, n_intervals: int = 1 << 62, dtype=np.float64):
     """Capped dyadic interval index from the float's exponent bits (sampler.py:111-124)."""
+    ud, scalar, host = _as_batch(u)
     if dtype == np.float32:
-        ud, scalar, host = _as_batch(u, torch.float32)
-        idx = kernels.dyadic_index32(ud, n_intervals)
+        idx = kernels.dyadic_index32(ud if not host else np.ascontiguousarray(ud, dtype=np.float32), n_intervals)
     else:
-        ud, scalar, host = _as_batch(u)
         idx = kernels.dyadic_index(ud, n_intervals)
     if scalar:
-        return int(idx[0])
-    return idx.cpu().numpy() if host else idx
+        return int(idx.reshape(-1)[0])
+    return idx.reshape(ud.shape) if host else idx
 
 
 def _eval_general_decay(table, ud: torch.Tensor) -> torch.Tensor:
@@ -100,22 +113,27 @@ def eval_dyadic(table, u, dtype=np.float64, out=None):
         if dtype == np.float32:
             raise ConfigError("the float32 fast path requires decay rate 1/2")
         ud, scalar, host = _as_batch(u)
-        return _result(_eval_general_decay(table, ud), scalar, host, out)
+        res = _eval_general_decay(table, dev.to_device(ud, torch.float64) if host else ud)
+        return _result(res.cpu().numpy().reshape(ud.shape) if host else res, scalar, host, out)
+    ud, scalar, host = _as_batch(u)
     if dtype == np.float32:
-        ud, scalar, host = _as_batch(u, torch.float32)
-        od = torch.empty_like(ud)
+        if host:
+            ud = np.ascontiguousarray(ud, dtype=np.float32)
+        else:
+            ud = ud.to(torch.float32)
+        od = _empty(ud, out)
         kernels.dyadic_eval32(table.coeffs32, ud, od)
     else:
-        ud, scalar, host = _as_batch(u)
-        od = torch.empty_like(ud)
+        od = _empty(ud, out)
         kernels.dyadic_eval(table.coeffs, ud, od)
     return _result(od, scalar, host, out)
 
 
 def eval_subdyadic(table: SubDyadicTable, u, out=None):
     """Octave x sub-interval table, float32 arithmetic (BASELINE.json config 2)."""
-    ud, scalar, host = _as_batch(u, torch.float32)
-    od = torch.empty_like(ud)
+    ud, scalar, host = _as_batch(u)
+    ud = np.ascontiguousarray(ud, dtype=np.float32) if host else ud.to(torch.float32)
+    od = _empty(ud, out)
     kernels.subdyadic_eval32(table.coeffs32, table.sub_bits, ud, od)
     return _result(od, scalar, host, out)
 
@@ -124,21 +142,25 @@ def eval_ncchi2(table, u, lam, out=None):
     """Approximate non-central chi-squared quantiles (sampler.py:175-193)."""
     ud, scalar, host = _as_batch(u)
     if dev.is_device_tensor(lam):
-        ld = lam.to(device=ud.device, dtype=torch.float64)
+        ld = lam.to(device=lam.device, dtype=torch.float64)
         if bool((ld < 0.0).any()):
             raise DomainError("lambda must be >= 0")
         lam_shape = tuple(ld.shape)
+        if host:
+            ud = dev.to_device(ud, torch.float64, ld.device)
+            host = False
     else:
         lam_arr = np.asarray(lam, dtype=np.float64)
         if np.any(lam_arr < 0.0):
             raise DomainError("lambda must be >= 0")
         lam_shape = lam_arr.shape
-        ld = dev.to_device(lam_arr.reshape(-1), torch.float64, ud.device)
+        ld = np.ascontiguousarray(lam_arr.reshape(-1)) if host else \
+            dev.to_device(lam_arr.reshape(-1), torch.float64, ud.device)
     if len(lam_shape) == 0:
         ld = ld.reshape(1)
-    elif ld.numel() != ud.numel() or (host and lam_shape != np.shape(np.atleast_1d(np.asarray(u)))):
+    elif tuple(lam_shape) != tuple(ud.shape):
         raise ConfigError("per-element lambda must match the shape of u")
-    od = torch.empty_like(ud)
+    od = _empty(ud, out)
     kernels.ncchi2_eval(table.eval_stacks, table.nu, ud, ld.reshape(-1), od)
     return _result(od, scalar, host, out)
 
@@ -166,9 +188,13 @@ def _is(obj, name, cls) -> bool:
 def gaussian_inv_cdf(u, out=None):
     """Exact AS241 quantile on the device (exact_dist.py:87-126), validating u."""
     ud, scalar, host = _as_batch(u)
-    if ud.numel() and bool(((~torch.isfinite(ud)) | (ud <= 0.0) | (ud >= 1.0)).any()):
+    if host:
+        bad = ud.size and bool(np.any(~np.isfinite(ud) | (ud <= 0.0) | (ud >= 1.0)))
+    else:
+        bad = ud.numel() and bool(((~torch.isfinite(ud)) | (ud <= 0.0) | (ud >= 1.0)).any())
+    if bad:
         raise DomainError("gaussian_inv_cdf requires 0 < u < 1")
-    od = torch.empty_like(ud)
+    od = _empty(ud, out)
     kernels.gaussian_inv_cdf(ud, od)
     return _result(od, scalar, host, out)
 

@@ -357,3 +357,130 @@ def test_level_statistics_match_path_moments(arv):
         assert st[k, 0] == n
         np.testing.assert_allclose(st[k, 1], d.mean(), rtol=1e-12, atol=1e-15)
         np.testing.assert_allclose(st[k, 2], ((d - d.mean()) ** 2).sum(), rtol=1e-9, atol=1e-18)
+
+
+# ----------------------------------------------------------------- round 2 --
+@pytest.fixture(scope="module")
+def golden_r2():
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_r2.npz")
+    with np.load(path) as z:
+        return {k: z[k] for k in z.files}
+
+
+def test_cir_exact_64knot_paths_match_reference(arv, golden_r2, hashes):
+    """BASELINE config 5's 64-knot table at levels 4 and 6 (16 and 64 steps),
+    per path against the reference's own simulate_cir_coupled(cir_exact)
+    (make_golden_r2.py): approximate side bit-exact, exact side through the
+    device quantile vs CDFLIB Newton (both meet |F - u| <= tol_f)."""
+    tab = arv.load_table("ncchi2_cir_k64_stacks")
+    for level, n0, n in hashes["cir_exact64_cases"]:
+        spec = arv.LevelSpec(level=level, scheme="cir_exact", process=arv.CirParams(**CIR), rv_source=tab,
+                             kind="four_way", n0=n0)
+        b = arv.simulate(spec, arv.level_stream(42, level), n)
+        ref = golden_r2[f"cir_exact64_l{level}_n{n0}"]
+        assert np.array_equal(bits(b.p_fine_approx.cpu().numpy()), bits(ref[1])), level
+        assert np.array_equal(bits(b.p_coarse_approx.cpu().numpy()), bits(ref[1])), level  # coarse repeats fine
+        # Each of the 16 / 64 exact transitions meets |F - u| <= tol_f (up to
+        # 1e-9, exact_dist.py:454-460) on both sides, with different iterates:
+        # per step the states differ by ~tol_f / (x f(x)) ~ 1e-9 relative and
+        # the differences propagate along the path (measured: one path of 256
+        # at 1.1e-7 after 16 steps, the median far below).
+        got = b.p_fine_exact.cpu().numpy()
+        np.testing.assert_allclose(got, ref[0], rtol=1e-6)
+        assert float(np.median(np.abs(got / ref[0] - 1.0))) < 1e-8, level
+
+
+def test_gbm_cubic_table_paths_match_reference(arv, golden_r2, hashes):
+    """The cubic K15 table (dyadic_eval, m = 3) through the GBM level kernels,
+    EM and Milstein, identity and call payoffs, per path vs the reference."""
+    cub = arv.load_table("dyadic_cubic_k15")
+    for scheme, payoff, level, n0 in hashes["gbm_cubic_cases"]:
+        spec = arv.LevelSpec(level=level, scheme=scheme, process=arv.GbmParams(**GBM), rv_source=cub,
+                             kind="four_way", payoff=payoff, strike=1.0, n0=n0)
+        b = arv.simulate(spec, arv.level_stream(42, level, 1), 512)
+        got = torch.stack([b.p_fine_exact, b.p_coarse_exact, b.p_fine_approx, b.p_coarse_approx]).cpu().numpy()
+        ref = golden_r2[f"gbm_cubic_{scheme}_{payoff}_l{level}_n{n0}"]
+        assert np.array_equal(bits(got[2:]), bits(ref[2:])), (scheme, payoff, level, n0)
+        np.testing.assert_allclose(got[:2], ref[:2], rtol=1e-13, atol=1e-15)
+
+
+@pytest.mark.parametrize("level,n0", [(0, 1), (1, 1), (4, 1), (3, 3), (6, 1)])
+def test_cir_milstein_paths_match_oracle(arv, orc, tables_npz, level, n0):
+    """cir_milstein_truncated (new: BASELINE config 5 names Milstein, the
+    reference has only truncated Euler) per path against the oracle
+    restatement (oracle.c orc_cir_paths, itself pinned to a numpy restatement
+    of mlmc.py:289-331 in test_oracle.py): approx side bit-exact, exact side
+    through AS241 tails <= 1e-13; ragged shard of the path range."""
+    lin = arv.load_table("dyadic_linear_k15")
+    spec = arv.LevelSpec(level=level, scheme="cir_milstein_truncated", process=arv.CirParams(**CIR),
+                         rv_source=lin, kind="four_way", n0=n0)
+    n = 1500
+    from paper_2012_09715_b200.mlmc import run_level
+
+    _, paths, _ = run_level(spec, arv.level_stream(42, level, 5), n, path_lo=333, path_count=1001,
+                            want_paths=True)
+    ref = np.stack(orc.cir_euler_paths(kappa=0.5, theta=0.04, sigma=0.2, x0=0.04, t_end=1.0, level=level, n0=n0,
+                                       payoff_call=False, strike=1.0, coeffs=tables_npz["dyadic_linear_k15"],
+                                       seed=42, seq=(level << 32) | 5, n_paths=n, path_lo=333, path_hi=1334,
+                                       milstein=True))
+    got = paths.cpu().numpy()
+    assert np.array_equal(bits(got[2:]), bits(ref[2:]))
+    np.testing.assert_allclose(got[:2], ref[:2], rtol=1e-13, atol=1e-15)
+
+
+def _two_way_slope(arv, scheme, levels, n):
+    lin = arv.load_table("dyadic_linear_k15")
+    v = []
+    for level in levels:
+        spec = arv.LevelSpec(level=level, scheme=scheme, process=arv.CirParams(**CIR), rv_source=lin,
+                             kind="four_way", n0=1)
+        v.append(arv.estimate_level_suite(spec, arv.level_stream(42, level), n)["two_way_exact"].variance)
+    return np.polyfit(levels, np.log2(v), 1)[0], v
+
+
+def test_cir_milstein_strong_convergence(arv):
+    """Strong order: the fine - coarse variance decays ~2^-2l under Milstein
+    against ~2^-l under truncated Euler (test_mlmc.py:82-89 is the reference's
+    slope check for Euler-Maruyama GBM, -1 +- 0.2)."""
+    levels = [2, 3, 4, 5, 6]
+    s_eul, v_eul = _two_way_slope(arv, "cir_euler_truncated", levels, 1 << 20)
+    s_mil, v_mil = _two_way_slope(arv, "cir_milstein_truncated", levels, 1 << 20)
+    assert -1.25 < s_eul < -0.75, (s_eul, v_eul)
+    assert s_mil < -1.6, (s_mil, v_mil)
+    assert v_mil[-1] < v_eul[-1] / 8
+
+
+def test_sides_semantics(arv, hashes):
+    """mlmc.py:156-229: unrequested sides are None; an approx side of an
+    'exact' source is a ConfigError; the requested side is unchanged."""
+    lin = arv.load_table("dyadic_linear_k15")
+    spec = arv.LevelSpec(level=2, scheme="euler_maruyama", process=arv.GbmParams(**GBM), rv_source=lin,
+                         kind="four_way", n0=1)
+    both = arv.simulate(spec, arv.level_stream(42, 2), 256)
+    for sides in ("exact", "approx"):
+        b = arv.simulate(spec, arv.level_stream(42, 2), 256, sides=sides)
+        present = [getattr(b, f) is not None for f in ("p_fine_exact", "p_coarse_exact", "p_fine_approx",
+                                                        "p_coarse_approx")]
+        assert present == hashes[f"sides_{sides}_present"], sides
+        for f in ("p_fine_exact", "p_coarse_exact", "p_fine_approx", "p_coarse_approx"):
+            if getattr(b, f) is not None:
+                assert torch.equal(getattr(b, f), getattr(both, f)), (sides, f)
+    ex = arv.LevelSpec(level=2, scheme="euler_maruyama", process=arv.GbmParams(**GBM), rv_source="exact",
+                       kind="two_way", n0=1)
+    b = arv.simulate(ex, arv.level_stream(42, 2), 256)  # default sides: exact
+    assert b.p_fine_approx is None and b.p_coarse_approx is None
+    assert torch.equal(b.p_fine_exact, both.p_fine_exact)
+    with pytest.raises(arv.ConfigError):
+        arv.simulate(ex, arv.level_stream(42, 2), 256, sides="both")
+    with pytest.raises(arv.ConfigError):
+        arv.simulate(spec, arv.level_stream(42, 2), 256, sides="neither")
+    # cir_exact: approx-only paths equal the approx side of a both-sides run
+    tab = arv.load_table("ncchi2_cir_k64_stacks")
+    cs = arv.LevelSpec(level=3, scheme="cir_exact", process=arv.CirParams(**CIR), rv_source=tab,
+                       kind="two_way", n0=1)
+    a = arv.simulate(cs, arv.level_stream(42, 3), 4096)  # two_way + table -> approx
+    assert a.p_fine_exact is None
+    full = arv.simulate(cs, arv.level_stream(42, 3), 4096, sides="both")
+    assert torch.equal(a.p_fine_approx, full.p_fine_approx)

@@ -224,3 +224,47 @@ class TestMlmcRestatement:
             assert np.array_equal(bits(xa), bits(ref[1]))
             np.testing.assert_allclose(xe, ref[0], rtol=1e-12)
             assert worst <= 1e-8
+
+    @pytest.mark.parametrize("level,n0", [(0, 1), (1, 1), (3, 1), (2, 3)])
+    def test_cir_milstein_restatement(self, orc, tables_npz, level, n0):
+        """The oracle's truncated-Milstein CIR (no reference counterpart, SURVEY
+        §8c "unpinned") against a numpy restatement built from the reference's
+        own truncated-Euler loop (mlmc.py:289-331: uniforms, coupling, payoffs)
+        with the Milstein term 1/2 b b'(dW^2 - dt) = sigma^2/4 (dW^2 - dt) of
+        b(x) = sigma sqrt(x) added after the Euler step.  Same operation order,
+        so both sides agree bit for bit; with the term removed it is the
+        reference's scheme (pinned in test_cir_euler_paths)."""
+        lin = tables_npz["dyadic_linear_k15"]
+        kp, th, sg, x0 = 0.5, 0.04, 0.2, 0.04
+        n, seq = 300, (level << 32) | 5
+        got = np.stack(orc.cir_euler_paths(kappa=kp, theta=th, sigma=sg, x0=x0, t_end=1.0, level=level, n0=n0,
+                                           payoff_call=False, strike=1.0, coeffs=lin, seed=42, seq=seq,
+                                           n_paths=n, milstein=True))
+        nf = n0 << level
+        dt = 1.0 / nf
+        sq = np.sqrt(dt)
+        u = orc.u32_to_f64(orc.pcg32_words(42, seq, 0, nf * n)).reshape(nf, n)  # word k n_paths + p
+
+        def step(x, dw, h):
+            r = x + kp * (th - x) * h + sg * np.sqrt(np.abs(x)) * dw  # mlmc.py:295-296
+            return r + 0.25 * sg * sg * (dw * dw - h)
+
+        xs = {k: np.full(n, x0) for k in ("fe", "ce", "fa", "ca")}
+        for pair in range(nf // 2):
+            z1, z2 = orc.as241_f64(u[2 * pair]), orc.as241_f64(u[2 * pair + 1])
+            w1, w2 = orc.dyadic_eval(lin, u[2 * pair]), orc.dyadic_eval(lin, u[2 * pair + 1])
+            xs["fe"] = step(step(xs["fe"], sq * z1, dt), sq * z2, dt)
+            xs["ce"] = step(xs["ce"], sq * (z1 + z2), 2.0 * dt)
+            xs["fa"] = step(step(xs["fa"], sq * w1, dt), sq * w2, dt)
+            xs["ca"] = step(xs["ca"], sq * (w1 + w2), 2.0 * dt)
+        if nf % 2:
+            xs["fe"] = step(xs["fe"], sq * orc.as241_f64(u[-1]), dt)
+            xs["fa"] = step(xs["fa"], sq * orc.dyadic_eval(lin, u[-1]), dt)
+        zero = np.zeros(n)
+        want = np.stack([xs["fe"], xs["ce"] if level else zero, xs["fa"], xs["ca"] if level else zero])
+        assert np.array_equal(bits(got), bits(want))
+        # and it is not the Euler scheme
+        eul = np.stack(orc.cir_euler_paths(kappa=kp, theta=th, sigma=sg, x0=x0, t_end=1.0, level=level, n0=n0,
+                                           payoff_call=False, strike=1.0, coeffs=lin, seed=42, seq=seq,
+                                           n_paths=n))
+        assert not np.array_equal(eul[0], got[0])
