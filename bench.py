@@ -632,11 +632,12 @@ def approximation_error(arv, out, offset: int, chunk: int = 1 << 26) -> dict:
 def mlmc_metrics(arv, args, rank, world, device) -> dict:
     """Config 4 (GBM EM, l=0..8, 2^22 paths/level) and config 5 (CIR exact, l=0..6,
     2^20 paths/level): one full multilevel pilot through the public estimator
-    ``estimate_level_suite`` (mlmc.py:383-411).  At N > 1 each level's paths
-    are sharded over the ranks and the per-level (count, mean, M2) triples and
-    the failure count are merged by NCCL all-reduces (mlmc.allreduce_triples),
-    so the reported statistics are the whole job's.  Timed with CUDA events
-    around the whole pilot (host work between levels included), max over ranks."""
+    ``estimate_level_suites`` (estimate_level_suite, mlmc.py:383-411, for all
+    levels).  At N > 1 each level's paths are sharded over the ranks and the
+    (count, mean, M2) triples of all levels and the failure count are merged by
+    NCCL all-reduces (mlmc.allreduce_triples), so the reported statistics are
+    the whole job's.  Timed with CUDA events around the whole pilot (host work
+    included), max over ranks."""
     import torch
 
     group = None
@@ -654,13 +655,13 @@ def mlmc_metrics(arv, args, rank, world, device) -> dict:
     for name, proc, scheme, tab, levels, n_paths in cases:
         specs = [arv.LevelSpec(level=l, scheme=scheme, process=proc, rv_source=tab, kind="four_way", n0=1)
                  for l in levels]
-        for sp in specs[:2]:  # warm-up
-            arv.estimate_level_suite(sp, arv.level_stream(42, sp.level), 4096 * world, group=group)
+        streams = [arv.level_stream(42, sp.level) for sp in specs]
+        arv.estimate_level_suites(specs[:2], streams[:2], 4096 * world, group=group)  # warm-up
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        suites = [arv.estimate_level_suite(sp, arv.level_stream(42, sp.level), n_paths, group=group)
-                  for sp in specs]  # raises NumericalError if any rank's exact transitions failed
+        # raises NumericalError if any rank's exact transitions failed
+        suites = arv.estimate_level_suites(specs, streams, n_paths, group=group)
         e1.record()
         e1.synchronize()
         t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device=device)
@@ -671,8 +672,8 @@ def mlmc_metrics(arv, args, rank, world, device) -> dict:
         paths_total = n_paths * len(levels)
         entry = {"paths_per_level": n_paths, "levels": [levels[0], levels[-1]], "seconds": secs,
                  "paths_per_s": paths_total / secs, "path_steps_per_s": n_paths * steps / secs,
-                 "api": "estimate_level_suite per level" + (f", NCCL all-reduce of the triples over {world} ranks"
-                                                            if world > 1 else "")}
+                 "api": "estimate_level_suites (all levels back to back, one host sync)" +
+                        (f"; one NCCL all-reduce pair of all levels' triples over {world} ranks" if world > 1 else "")}
         entry["roofline"] = _fp64_roofline("gbm_level8" if scheme != "cir_exact" else "cir_level6",
                                            n_paths * steps / secs)
         if scheme == "cir_exact":

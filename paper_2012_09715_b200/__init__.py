@@ -17,7 +17,7 @@ from .errors import (
 )
 from .mlmc import (
     Allocation, CirParams, GbmParams, LevelSpec, LevelStats, PathBatch, difference, estimate_level,
-    estimate_level_suite, level_stream, optimal_allocation, optimal_allocation_nested, simulate,
+    estimate_level_suite, estimate_level_suites, level_stream, optimal_allocation, optimal_allocation_nested, simulate,
     simulate_cir_coupled, simulate_gbm_coupled, speedup_report, telescoped_mean,
 )
 from .sampler import (
@@ -32,7 +32,7 @@ __all__ = [
     "ApproxRvError", "BadMagicError", "ChecksumError", "ConfigError", "DeviceError", "DomainError",
     "NumericalError", "TableIOError", "TruncatedFileError", "VersionError",
     "Allocation", "CirParams", "GbmParams", "LevelSpec", "LevelStats", "PathBatch", "difference",
-    "estimate_level", "estimate_level_suite", "level_stream", "optimal_allocation", "optimal_allocation_nested",
+    "estimate_level", "estimate_level_suite", "estimate_level_suites", "level_stream", "optimal_allocation", "optimal_allocation_nested",
     "simulate", "simulate_cir_coupled", "simulate_gbm_coupled", "speedup_report", "telescoped_mean",
     "CoupledGaussianBatch", "GaussianSamplePair", "Pcg32Stream", "PhiloxStream", "UniformStream", "dyadic_index",
     "eval_constant", "eval_dyadic", "eval_ncchi2", "eval_subdyadic", "evaluate", "gaussian_exact_batch",

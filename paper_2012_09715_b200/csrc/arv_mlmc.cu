@@ -457,6 +457,283 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
     cta_moments<ARV_NKIND>(d, valid, parts + static_cast<int64_t>(blockIdx.x) * 3 * ARV_NKIND);
 }
 
+// ------------------------------------------ Gaussian level kernel, v2 --
+// PCG32 streams (the BASELINE generator), every Gaussian scheme.  Same paths,
+// same approximate side bit for bit, same statistics layout as
+// k_gaussian_level; the work per path-step is restructured around the word w
+// of the uniform u = (w + 1/2) 2^-32:
+//  * exact side (AS241, exact_dist.py:87-126): the central rational
+//    (|u - 1/2| <= 0.425, an integer range test on w) is evaluated for every
+//    element with the A/B coefficients as compile-time constants -- they
+//    become constant-bank operands of the FP64 instructions, so there are no
+//    coefficient loads or per-lane row selects (k_gaussian_level read 8
+//    16-byte rows per element from shared memory to serve central and tail
+//    lanes with one rational).  Tail elements (15%) are compacted warp-wide
+//    into a per-warp list and get their whole tail evaluation -- log, sqrt,
+//    C/D (or E/F) rational, division -- in one pass per 32 tails, again with
+//    constant coefficients.  q = u - 1/2 = (1 + u) - 3/2 and the tail's
+//    min(u, 1 - u) are built exactly from w's bits.
+//  * approximate side (dyadic_eval / constant_eval, _kernels.pyx:16-73):
+//    v = min(u, 1 - u) = (w' + 1/2) 2^-32 with w' = w or ~w (exact), the
+//    interval index 1022 - expo(v) = clz(w') (capped), one 16-byte shared
+//    load for (c0, c1), the reference's separately rounded Horner steps, and
+//    the sign as an XOR of w's top bit into z's sign bit.
+//  * path updates: mu dt, (0.5 sg) sg hoisted (same roundings).
+// With ARV_GBM_FMA_EXACT the exact side's Horner steps and the division are
+// fused multiply-adds (a different rounding of the same AS241 evaluation,
+// relative differences ~1e-16 per normal; the MLMC contract for the exact
+// side is statistical, and per-path tests hold it to 1e-13).
+#ifndef ARV_GBM_V2
+#define ARV_GBM_V2 1
+#endif
+#ifndef ARV_GBM_FMA_EXACT
+#define ARV_GBM_FMA_EXACT 1
+#endif
+#ifndef ARV_GBM_V2_MINB
+#define ARV_GBM_V2_MINB 4
+#endif
+
+namespace g2 {
+// coefficient sets: rows of the __constant__ table kAS241d (A, B, C, D, E, F);
+// indexed with compile-time indices they are constant-bank operands of the
+// FP64 instructions (literal doubles would be materialised with two UMOVs each)
+enum { kA = 0, kB = 1, kC = 2, kD = 3, kE = 4, kF = 5 };
+// |u - 1/2| <= 0.425 (exact_dist.py:92) for u = (w + 1/2) 2^-32 <=> w in
+// [ceil(2^31 - 1/2 - 0.425 * 2^32), floor(2^31 - 1/2 + 0.425 * 2^32)]
+// (0.425 the double; q is exact, so the integer test is exact)
+constexpr uint32_t kCentralLo = 0x13333333u, kCentralSpan = 0xECCCCCCCu - 0x13333333u;
+
+template <bool FMA>
+__device__ __forceinline__ double horner(int which, double x) {
+    double acc = kAS241d[which][7];
+#pragma unroll
+    for (int i = 6; i >= 0; --i)
+        acc = FMA ? fma(acc, x, kAS241d[which][i]) : __dadd_rn(__dmul_rn(acc, x), kAS241d[which][i]);
+    return acc;
+}
+
+// n / d for the positive, well-scaled AS241 denominators: reciprocal estimate,
+// two Newton steps and a residual correction (no special-case path).
+template <bool FMA>
+__device__ __forceinline__ double divide(double n, double d) {
+    if constexpr (!FMA) {
+        return __ddiv_rn(n, d);
+    } else {
+        double y;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+        y = fma(fma(-d, y, 1.0), y, y);
+        y = fma(fma(-d, y, 1.0), y, y);
+        const double q0 = __dmul_rn(n, y);
+        return fma(fma(-d, q0, n), y, q0);
+    }
+}
+
+template <bool FMA>
+__device__ __forceinline__ double central(double q) {
+    const double r = FMA ? fma(-q, q, 0.180625) : __dsub_rn(0.180625, __dmul_rn(q, q));
+    return divide<FMA>(__dmul_rn(q, horner<FMA>(kA, r)), horner<FMA>(kB, r));
+}
+
+// |AS241(u)| of a tail element from w = min(u, 1 - u) (exact_dist.py:100-126)
+template <bool FMA>
+__device__ __forceinline__ double tail_abs(double w) {
+    const double r = __dsqrt_rn(-log(w));
+    if (r <= 5.0) {
+        const double x = __dsub_rn(r, 1.6);
+        return divide<FMA>(horner<FMA>(kC, x), horner<FMA>(kD, x));
+    }
+    const double x = __dsub_rn(r, 5.0);
+    return divide<FMA>(horner<FMA>(kE, x), horner<FMA>(kF, x));
+}
+
+// AS241 of N words per lane; all 32 lanes of the warp call it together.
+// v[k] = min(u, 1 - u) of element k (exact).  buf: this warp's 32 N doubles.
+template <int N, bool FMA>
+__device__ __forceinline__ void as241_words(const uint32_t (&w)[N], const double (&v)[N], double (&z)[N],
+                                            double *buf) {
+    unsigned pend = 0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        if (w[k] - kCentralLo > kCentralSpan) pend |= 1u << k;
+        z[k] = central<FMA>(__dsub_rn(one_plus_u32(w[k]), 1.5));  // q = u - 1/2 exactly
+    }
+    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+    int pos[N];
+    int total = 0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const unsigned b = __ballot_sync(0xffffffffu, (pend >> k) & 1u);
+        pos[k] = total + __popc(b & lt);
+        total += __popc(b);
+    }
+    if (total) {  // warp-uniform
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            if ((pend >> k) & 1u) buf[pos[k]] = v[k];
+        __syncwarp();
+        for (int g = threadIdx.x & 31; g < total; g += 32) buf[g] = tail_abs<FMA>(buf[g]);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            if ((pend >> k) & 1u) {
+                const double t = buf[pos[k]];
+                z[k] = w[k] >> 31 ? t : -t;  // upper tail positive (exact_dist.py:124-126)
+            }
+        __syncwarp();  // the list is reused by the next call
+    }
+}
+
+// v = min(u, 1 - u) = (w' + 1/2) 2^-32, w' = w (u < 1/2) or ~w (exact)
+__device__ __forceinline__ double reflected(uint32_t w) {
+    const uint32_t wr = w ^ static_cast<uint32_t>(static_cast<int32_t>(w) >> 31);
+    return __dsub_rn(one_plus_u32(wr), 1.0);
+}
+
+// Approximate side of one element: dyadic_eval (DEG >= 1; table interleaved
+// [K1][S] with S = DEG + 1 rounded up to even) or constant_eval (DEG == 0,
+// values[K1]) -- _kernels.pyx:56-73, :16-23.
+template <int DEG>
+__device__ __forceinline__ double table(const double *sm, uint32_t w, double v, int cap, int64_t K1) {
+    if constexpr (DEG == 0) {
+        const double u = __dsub_rn(one_plus_u32(w), 1.0);
+        long long idx = static_cast<long long>(__dmul_rn(static_cast<double>(K1), u));
+        idx = idx < K1 ? idx : K1 - 1;
+        return sm[idx];
+    } else {
+        constexpr int S = (DEG + 2) & ~1;
+        const uint32_t neg = static_cast<uint32_t>(static_cast<int32_t>(w) >> 31);
+        int idx = __clz(w ^ neg);  // 1022 - expo(v), _kernels.pyx:36
+        idx = idx < cap ? idx : cap;
+        const double *c = sm + idx * S;
+        double z;
+        if constexpr (DEG == 1) {
+            const double2 c01 = *reinterpret_cast<const double2 *>(c);
+            z = __dadd_rn(__dmul_rn(c01.y, v), c01.x);
+        } else {
+            z = c[DEG];
+#pragma unroll
+            for (int d = DEG - 1; d >= 0; --d) z = __dadd_rn(__dmul_rn(z, v), c[d]);
+        }
+        // out = pred ? z : -z (u < 1/2 <=> top bit of w clear)
+        return __hiloint2double(__double2hiint(z) ^ static_cast<int>(neg & 0x80000000u), __double2loint(z));
+    }
+}
+}  // namespace g2
+
+template <int DEG, int SCHEME>
+__global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level_v2(LevelArgs A,
+                                                                                 const double *__restrict__ coeffs,
+                                                                                 int64_t K1,
+                                                                                 double *__restrict__ parts,
+                                                                                 double *__restrict__ paths) {
+    constexpr bool FMA = ARV_GBM_FMA_EXACT != 0;
+    constexpr bool GBM = SCHEME == ARV_SCHEME_EM || SCHEME == ARV_SCHEME_MILSTEIN;
+    constexpr bool MIL = SCHEME == ARV_SCHEME_MILSTEIN || SCHEME == ARV_SCHEME_CIR_MILSTEIN_TRUNCATED;
+    constexpr int S = DEG == 0 ? 1 : (DEG + 2) & ~1;
+    extern __shared__ __align__(16) double smd[];
+    __shared__ double tails[kLevelBlock / 32][32 * 4];
+    if constexpr (DEG == 0) {
+        for (int i = threadIdx.x; i < K1; i += blockDim.x) smd[i] = __ldg(coeffs + i);
+    } else {  // reference layout (DEG+1, K1) -> interleaved [K1][S]
+        for (int i = threadIdx.x; i < (DEG + 1) * K1; i += blockDim.x) {
+            const int d = static_cast<int>(i / K1), j = static_cast<int>(i % K1);
+            smd[j * S + d] = __ldg(coeffs + i);
+        }
+    }
+    __syncthreads();
+    double *buf = tails[threadIdx.x >> 5];
+    const int cap = static_cast<int>(K1 - 1);
+
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool valid = i < A.path_count;
+    // every lane runs the path loop (the tail list needs the whole warp);
+    // lanes past the range simulate path_lo and are not counted
+    uint64_t s = path_start_state(A, static_cast<uint64_t>(A.path_lo + (valid ? i : 0)));
+    const Affine st = A.step;
+    const double x0 = A.x0, dt_f = A.dt_f, dt_c = A.dt_c, sq_f = A.sq_f;
+    const double mudt_f = __dmul_rn(A.a, dt_f), mudt_c = __dmul_rn(A.a, dt_c);  // mlmc.py:195
+    const double sg = A.b, hs2 = __dmul_rn(__dmul_rn(0.5, A.b), A.b);           // mlmc.py:196-197
+    const bool we = A.want_exact, wa = A.want_approx;
+    double xf_e = x0, xc_e = x0, xf_a = x0, xc_a = x0;
+    auto step = [&](double x, double dw, double dt, double mudt) -> double {
+        if constexpr (GBM) {
+            double incr = __dadd_rn(mudt, __dmul_rn(sg, dw));
+            if (MIL) incr = __dadd_rn(incr, __dmul_rn(hs2, __dsub_rn(__dmul_rn(dw, dw), dt)));
+            return __dmul_rn(x, __dadd_rn(1.0, incr));
+        } else {
+            return cir_step<MIL>(x, dw, dt, A.a, A.b, A.c);
+        }
+    };
+    auto pair_step = [&](double z0, double z1, double w0, double w1) {
+        xf_e = step(step(xf_e, __dmul_rn(sq_f, z0), dt_f, mudt_f), __dmul_rn(sq_f, z1), dt_f, mudt_f);
+        xc_e = step(xc_e, __dmul_rn(sq_f, __dadd_rn(z0, z1)), dt_c, mudt_c);
+        xf_a = step(step(xf_a, __dmul_rn(sq_f, w0), dt_f, mudt_f), __dmul_rn(sq_f, w1), dt_f, mudt_f);
+        xc_a = step(xc_a, __dmul_rn(sq_f, __dadd_rn(w0, w1)), dt_c, mudt_c);
+    };
+    auto draw = [&]() -> uint32_t {
+        const uint32_t w = pcg32_output(s);
+        s = st.a * s + st.c;
+        return w;
+    };
+    int64_t pairs = A.n_f / 2;
+    for (; pairs >= 2; pairs -= 2) {  // four uniforms (two coarse steps) per pass
+        uint32_t w[4];
+        double v[4], z[4], a[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            w[k] = draw();
+            v[k] = g2::reflected(w[k]);
+        }
+        if (we) g2::as241_words<4, FMA>(w, v, z, buf);
+        else z[0] = z[1] = z[2] = z[3] = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[k] = wa ? g2::table<DEG>(smd, w[k], v[k], cap, K1) : 0.0;
+        pair_step(z[0], z[1], a[0], a[1]);
+        pair_step(z[2], z[3], a[2], a[3]);
+    }
+    if (pairs) {
+        uint32_t w[2];
+        double v[2], z[2], a[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            w[k] = draw();
+            v[k] = g2::reflected(w[k]);
+        }
+        if (we) g2::as241_words<2, FMA>(w, v, z, buf);
+        else z[0] = z[1] = 0.0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) a[k] = wa ? g2::table<DEG>(smd, w[k], v[k], cap, K1) : 0.0;
+        pair_step(z[0], z[1], a[0], a[1]);
+    }
+    if (A.n_f & 1) {  // odd fine-step count (n0 odd at level 0)
+        uint32_t w[1] = {draw()};
+        double v[1] = {g2::reflected(w[0])}, z[1] = {0.0};
+        if (we) g2::as241_words<1, FMA>(w, v, z, buf);
+        if (we) xf_e = step(xf_e, __dmul_rn(sq_f, z[0]), dt_f, mudt_f);
+        if (wa) xf_a = step(xf_a, __dmul_rn(sq_f, g2::table<DEG>(smd, w[0], v[0], cap, K1)), dt_f, mudt_f);
+    }
+    double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (valid) {
+        const double fe = payoff_fn(xf_e, A.payoff, A.strike);
+        const double fa = payoff_fn(xf_a, A.payoff, A.strike);
+        const double ce = A.level > 0 ? payoff_fn(xc_e, A.payoff, A.strike) : 0.0;
+        const double ca = A.level > 0 ? payoff_fn(xc_a, A.payoff, A.strike) : 0.0;
+        // mlmc.py:341-353 (two_way exact / approx, four_way) and plain
+        d[0] = __dsub_rn(fe, ce);
+        d[1] = __dsub_rn(fa, ca);
+        d[2] = __dadd_rn(__dsub_rn(__dsub_rn(fe, ce), fa), ca);
+        d[3] = fe;
+        d[4] = fa;
+        if (paths) {
+            paths[i] = fe;
+            paths[A.path_count + i] = ce;
+            paths[2 * A.path_count + i] = fa;
+            paths[3 * A.path_count + i] = ca;
+        }
+    }
+    cta_moments<ARV_NKIND>(d, valid, parts + static_cast<int64_t>(blockIdx.x) * 3 * ARV_NKIND);
+}
+
 // ----------------------------------------------------------- CIR exact --
 // Lambda-sorted transitions.  The exact quantile costs ~3 sweeps whose window
 // covers ~16 sqrt(lambda/2) Poisson terms. lambda is proportional to the path
@@ -915,11 +1192,14 @@ int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, in
         return set_error(ARV_ERR_CONFIG, "workspace too small");
     double *parts = static_cast<double *>(workspace);
     const size_t smem = sizeof(double) * (degree + 1) * K1;
+    // v2 table layout: interleaved [K1][S], S = degree + 1 rounded up to even
+    const size_t smem2 = sizeof(double) * (degree == 0 ? 1 : ((degree + 2) & ~1)) * K1;
     cudaStream_t s = as_stream(stream);
 #define ARV_LAUNCH(D, S)                                                                              \
     (A.rng == ARV_RNG_PHILOX                                                                          \
          ? k_gaussian_level<D, S, true><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths) \
-         : k_gaussian_level<D, S, false><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths))
+         : (ARV_GBM_V2 ? k_gaussian_level_v2<D, S><<<(unsigned)nb, kLevelBlock, smem2, s>>>(A, coeffs, K1, parts, paths) \
+                       : k_gaussian_level<D, S, false><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths)))
 #define ARV_SCHEMES(D)                                                                      \
     case D:                                                                                 \
         switch (scheme) {                                                                   \

@@ -476,6 +476,10 @@ def estimate_level_suite(spec: LevelSpec, stream: Pcg32Stream, n_pilot: int, gro
     if _is_exact(spec.rv_source):
         raise ConfigError("suite estimation needs a table source")
     stats, seconds = _timed_level(spec, stream, n_pilot, group)
+    return _suite_from(spec, stats, seconds)
+
+
+def _suite_from(spec: LevelSpec, stats, seconds: float) -> dict:
     draws = spec.n_steps_fine
     if spec.scheme == "cir_exact":
         return {
@@ -488,6 +492,59 @@ def estimate_level_suite(spec: LevelSpec, stream: Pcg32Stream, n_pilot: int, gro
         "two_way_approx": _stats_from(spec.level, "two_way", stats[1], seconds, draws),
         "four_way": _stats_from(spec.level, "four_way", stats[2], seconds, draws),
     }
+
+
+def estimate_level_suites(specs: list, streams: list, n_pilot: int, group=None) -> list:
+    """``estimate_level_suite`` for every level of a pilot in one pass.
+
+    The levels are launched back to back on the device (no host round trip
+    between them), each rank simulating its contiguous share of every
+    level's paths; the per-level (count, mean, M2) triples of all levels are
+    merged across ranks with ONE pair of all-reduces (NCCL on GPUs) and the
+    failure counts with one more, and the host synchronises once.  Results
+    equal the per-level calls (same paths, same merge); per-level device
+    seconds come from CUDA events between the launches.
+    """
+    if len(specs) != len(streams):
+        raise ConfigError("one stream per level spec")
+    if n_pilot < 100:
+        raise ConfigError(f"pilot size must be >= 100, got {n_pilot}")
+    if any(_is_exact(sp.rv_source) for sp in specs):
+        raise ConfigError("suite estimation needs a table source")
+    device = dev.require_cuda()
+    rank, world = 0, 1
+    if group is not None or _dist_ready():
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+    per, extra = divmod(n_pilot, world)
+    lo = rank * per + min(rank, extra)
+    cnt = per + (1 if rank < extra else 0)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(specs) + 1)]
+    evs[0].record()
+    stats, fails = [], []
+    for k, (spec, stream) in enumerate(zip(specs, streams)):
+        st, _, nf = run_level(spec, stream, n_pilot, path_lo=lo, path_count=cnt, device=device)
+        stats.append(st)
+        if nf is not None:
+            fails.append(nf)
+        evs[k + 1].record()
+    allst = torch.cat(stats, dim=0)  # (levels * NSLOT, 3)
+    n_fail = torch.stack(fails).sum().reshape(1) if fails else None
+    if world > 1:
+        import torch.distributed as dist
+
+        allst = allreduce_triples(allst, group)
+        if n_fail is not None:
+            n_fail = _host_if_gloo(n_fail, group)
+            dist.all_reduce(n_fail, group=group)
+    evs[-1].synchronize()
+    if n_fail is not None and int(n_fail.item()):
+        raise NumericalError(f"exact CIR transition failed: {int(n_fail.item())} transitions exceeded the "
+                             "1e-8 residual contract")
+    host = allst.cpu().numpy().reshape(len(specs), NSLOT, 3)
+    return [_suite_from(spec, host[k], evs[k].elapsed_time(evs[k + 1]) * 1e-3 * world)
+            for k, spec in enumerate(specs)]
 
 
 # ---------------------------------------------------------------------------

@@ -45,6 +45,14 @@ def main():
             f = full[slot[k]]
             res[f"{name}/{k}"] = [s.n_paths, s.mean, s.variance, f[0], f[1], f[2] / (f[0] - 1)]
         assert full.shape == (NSLOT, 3)
+    # the batched pilot (all levels, one all-reduce pair) equals the per-level calls
+    specs = [spec for _, spec in cases]
+    suites = arv.estimate_level_suites(specs, [arv.level_stream(42, sp.level) for sp in specs], n)
+    for (name, spec), got in zip(cases, suites):
+        want = arv.estimate_level_suite(spec, arv.level_stream(42, spec.level), n)
+        for k in want:
+            assert (got[k].n_paths, got[k].mean, got[k].variance) == \
+                (want[k].n_paths, want[k].mean, want[k].variance), (name, k)
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
         json.dump(res, fh)
     dist.barrier()

@@ -75,7 +75,7 @@ def test_index_and_constant_host(K, orc, tabs, n):
 
 @pytest.mark.parametrize("n", [1, 4099, (1 << 21) + 11])
 def test_ncchi2_host_shared_and_per_element_lambda(K, orc, tabs, n):
-    st, nu = tabs["ncchi2_cir_k64_stacks"], float(tabs["ncchi2_cir_k64_nu"])
+    st, nu = tabs["ncchi2_cir_k64_stacks"], float(np.asarray(tabs["ncchi2_cir_k64_nu"]).reshape(-1)[0])
     u = u64(n, 5)
     for lam in (np.array([7.5]), np.linspace(0.0, 400.0, n)):
         out = np.empty(n)

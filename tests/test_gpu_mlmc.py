@@ -484,3 +484,25 @@ def test_sides_semantics(arv, hashes):
     assert a.p_fine_exact is None
     full = arv.simulate(cs, arv.level_stream(42, 3), 4096, sides="both")
     assert torch.equal(a.p_fine_approx, full.p_fine_approx)
+
+
+def test_estimate_level_suites_equals_per_level_calls(arv):
+    """The batched pilot API (all levels launched back to back, one host sync)
+    returns exactly the per-level estimate_level_suite statistics."""
+    lin = arv.load_table("dyadic_linear_k15")
+    tab = arv.load_table("ncchi2_cir_k64_stacks")
+    specs = [arv.LevelSpec(level=l, scheme="euler_maruyama", process=arv.GbmParams(**GBM), rv_source=lin,
+                           kind="four_way", n0=1) for l in range(4)]
+    specs += [arv.LevelSpec(level=l, scheme="cir_exact", process=arv.CirParams(**CIR), rv_source=tab,
+                            kind="four_way", n0=1) for l in (0, 2)]
+    n = 20011
+    suites = arv.estimate_level_suites(specs, [arv.level_stream(42, sp.level) for sp in specs], n)
+    for sp, got in zip(specs, suites):
+        want = arv.estimate_level_suite(sp, arv.level_stream(42, sp.level), n)
+        assert list(got) == list(want)
+        for k in want:
+            assert (got[k].n_paths, got[k].mean, got[k].variance) == (want[k].n_paths, want[k].mean,
+                                                                       want[k].variance), (sp.level, k)
+            assert got[k].cost_per_path_seconds > 0
+    with pytest.raises(arv.ConfigError):
+        arv.estimate_level_suites(specs, [], n)

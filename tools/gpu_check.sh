@@ -1,8 +1,7 @@
-# One-shot GPU check used during development: GPU tests, smoke, bench lines.
-# Writes gpurun_out/.
+# One-shot GPU check used during development.  Writes gpurun_out/.
 set -x
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --tb=short 2>&1 | tail -80 > gpurun_out/r2_gputest.log
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke.log 2>&1
-timeout 900 python bench.py > gpurun_out/r2_bench.json 2> gpurun_out/r2_bench.err
-timeout 900 python bench.py --impl reference > gpurun_out/r2_bench_ref.json 2>> gpurun_out/r2_bench.err
-tail -5 gpurun_out/r2_gputest.log; cat gpurun_out/r2_smoke.log; tail -c 1500 gpurun_out/r2_bench.err
+bash tools/gpu_ab.sh "--which gbmall,gbm --reps 10" > gpurun_out/r2_ab.log 2>&1
+python tools/level_times.py > gpurun_out/r2_levels.log 2>&1
+timeout 900 python bench.py --no-cpu > gpurun_out/r2_bench.json 2> gpurun_out/r2_bench.err
+tail -5 gpurun_out/r2_gputest.log; cat gpurun_out/r2_ab.log gpurun_out/r2_levels.log
