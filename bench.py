@@ -351,11 +351,28 @@ def config1_entry(arv, _native, device, offset: int, peak: float, steps: int = 2
     n, tname, wl = WORKLOADS["config1"]
     per_launch, launches, _ = time_generator(arv, _native, arv.load_table(tname), n, offset, steps, device)
     achieved = n * BYTES_PER_SAMPLE / per_launch / 1e9
+    # the same protocol for a store-only kernel of the same size: what a pure
+    # 64 MiB write achieves per launch (launch + ramp + drain included)
+    import torch
+
+    out = torch.empty(n, dtype=torch.float32, device=device)
+    scratch = torch.empty(128 << 20, dtype=torch.float32, device=device)
+    s = torch.cuda.current_stream().cuda_stream
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
+    for a, b in evs:
+        _native.call("arv_store_probe", scratch.data_ptr(), scratch.numel(), s)
+        a.record()
+        _native.call("arv_store_probe", out.data_ptr(), n, s)
+        b.record()
+    torch.cuda.synchronize()
+    probe = sum(a.elapsed_time(b) for a, b in evs) * 1e-3 / len(evs)
     return {"workload": wl, "value": n / per_launch, "unit": "samples/s", "us_per_launch": per_launch * 1e6,
             "steps": steps, "gpu_launches": int(launches),
             "l2": "output < L2: each launch timed alone, 512 MiB store sweep flushes L2 in between",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "algorithmic_bytes_per_launch": n * BYTES_PER_SAMPLE}}
+                         "algorithmic_bytes_per_launch": n * BYTES_PER_SAMPLE,
+                         "store_probe_same_size_us": probe * 1e6,
+                         "frac_of_store_probe_same_size": probe / per_launch}}
 
 
 def e2e_plugin(arv, device, steps: int = 3) -> dict:
@@ -656,7 +673,8 @@ def mlmc_metrics(arv, args, rank, world, device) -> dict:
         specs = [arv.LevelSpec(level=l, scheme=scheme, process=proc, rv_source=tab, kind="four_way", n0=1)
                  for l in levels]
         streams = [arv.level_stream(42, sp.level) for sp in specs]
-        arv.estimate_level_suites(specs[:2], streams[:2], 4096 * world, group=group)  # warm-up
+        # warm-up: one untimed full pilot (workspace allocations, module loads)
+        arv.estimate_level_suites(specs, streams, n_paths, group=group)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()

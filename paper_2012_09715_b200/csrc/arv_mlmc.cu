@@ -644,11 +644,47 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
     double *buf = tails[threadIdx.x >> 5];
     const int cap = static_cast<int>(K1 - 1);
 
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // Persistent tiles: the grid is one wave of resident CTAs, and CTA b
+    // simulates tiles b, b + G, b + 2G, ... of 256 paths (tile t = paths
+    // path_lo + 256 t + [0, 256)), writing tile t's partial exactly as the
+    // one-tile-per-CTA form did: same partition, same statistics bit for bit.
+    // The table, the lane maps and the tile start are set up once per CTA
+    // instead of once per 256 paths; path p's PCG32 state is LCG^lane applied
+    // to the tile's start state (a per-lane map staged in shared memory, the
+    // tile start advanced by one map per tile) instead of a walk over the bits
+    // of p per thread.
+    // lane maps and the tile-to-tile map live in shared memory (re-read once
+    // per tile) so that they do not hold registers across the path loop
+    __shared__ Affine lane_map[kLevelBlock + 1];  // [kLevelBlock]: tile -> next tile of this CTA
+    {
+        Affine m{1, 0};
+        const unsigned t = threadIdx.x;
+        for (int b = 0; b < 8; ++b)
+            if ((t >> b) & 1u) m = {A.jump2[b].a * m.a, A.jump2[b].a * m.c + A.jump2[b].c};
+        lane_map[t] = m;
+        if (t == 0) {
+            Affine g{1, 0};
+            const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kLevelBlock;
+            for (int b = 0; b < kPathJumpBits; ++b)
+                if ((stride >> b) & 1u) g = {A.jump2[b].a * g.a, A.jump2[b].a * g.c + A.jump2[b].c};
+            lane_map[kLevelBlock] = g;
+        }
+    }
+    const int64_t ntiles = (A.path_count + kLevelBlock - 1) / kLevelBlock;
+    // start state of this CTA's current tile
+    uint64_t tile_s = path_start_state(A, static_cast<uint64_t>(A.path_lo) + static_cast<uint64_t>(blockIdx.x) * kLevelBlock);
+    __syncthreads();
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i = tile * kLevelBlock + threadIdx.x;
     const bool valid = i < A.path_count;
     // every lane runs the path loop (the tail list needs the whole warp);
-    // lanes past the range simulate path_lo and are not counted
-    uint64_t s = path_start_state(A, static_cast<uint64_t>(A.path_lo + (valid ? i : 0)));
+    // lanes past the range simulate a path beyond it and are not counted
+    uint64_t s;
+    {
+        const Affine my = lane_map[threadIdx.x], nx = lane_map[kLevelBlock];
+        s = my.a * tile_s + my.c;
+        tile_s = nx.a * tile_s + nx.c;
+    }
     const Affine st = A.step;
     const double x0 = A.x0, dt_f = A.dt_f, dt_c = A.dt_c, sq_f = A.sq_f;
     const double mudt_f = __dmul_rn(A.a, dt_f), mudt_c = __dmul_rn(A.a, dt_c);  // mlmc.py:195
@@ -731,7 +767,8 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
             paths[3 * A.path_count + i] = ca;
         }
     }
-    cta_moments<ARV_NKIND>(d, valid, parts + static_cast<int64_t>(blockIdx.x) * 3 * ARV_NKIND);
+    cta_moments<ARV_NKIND>(d, valid, parts + tile * 3 * ARV_NKIND);
+    }
 }
 
 // ----------------------------------------------------------- CIR exact --
@@ -1169,6 +1206,15 @@ int64_t arv_mlmc_cir_workspace_bytes(int64_t path_count) {
     return CirWs(path_count < 1 ? 1 : path_count, nullptr).total;
 }
 
+// one wave of resident CTAs (at most one per tile)
+#ifndef ARV_GBM_V2_WAVES
+#define ARV_GBM_V2_WAVES 8  // waves of the grid: 1 -> 5.97 ms at level 8, 2 -> 5.69, 8 -> 5.55 (dynamic CTA scheduling still pays)
+#endif
+static unsigned grid_v2(const void *fn, int64_t tiles, size_t smem) {
+    const int64_t wave = static_cast<int64_t>(resident_ctas(fn, kLevelBlock, smem)) * device_sm_count() * ARV_GBM_V2_WAVES;
+    return static_cast<unsigned>(tiles < wave ? tiles : wave);
+}
+
 int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, int degree, int64_t K1, double *stats,
                             double *paths, void *workspace, int64_t workspace_bytes, void *stream) {
     LevelArgs A;
@@ -1198,7 +1244,8 @@ int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, in
 #define ARV_LAUNCH(D, S)                                                                              \
     (A.rng == ARV_RNG_PHILOX                                                                          \
          ? k_gaussian_level<D, S, true><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths) \
-         : (ARV_GBM_V2 ? k_gaussian_level_v2<D, S><<<(unsigned)nb, kLevelBlock, smem2, s>>>(A, coeffs, K1, parts, paths) \
+         : (ARV_GBM_V2 ? k_gaussian_level_v2<D, S><<<grid_v2((const void *)k_gaussian_level_v2<D, S>, nb, smem2), \
+                                                      kLevelBlock, smem2, s>>>(A, coeffs, K1, parts, paths)             \
                        : k_gaussian_level<D, S, false><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths)))
 #define ARV_SCHEMES(D)                                                                      \
     case D:                                                                                 \

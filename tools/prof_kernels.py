@@ -98,6 +98,12 @@ def main():
         sp = arv.LevelSpec(level=8, scheme="euler_maruyama", process=arv.GbmParams(0.05, 0.2, 1.0, 1.0),
                            rv_source=lin, kind="four_way", n0=1)
         res["gbm_l8"] = timed(lambda: run_level(sp, arv.level_stream(42, 8), 1 << 22), args.reps)
+    if "gbml01" in which:  # levels 0 and 1 of config 4 (per-level fixed cost)
+        lin = arv.load_table("dyadic_linear_k15")
+        for lv in (0, 1):
+            sp = arv.LevelSpec(level=lv, scheme="euler_maruyama", process=arv.GbmParams(0.05, 0.2, 1.0, 1.0),
+                               rv_source=lin, kind="four_way", n0=1)
+            res[f"gbm_l{lv}"] = timed(lambda: run_level(sp, arv.level_stream(42, lv), 1 << 22), args.reps)
     if "gbmall" in which:  # config 4: levels 0..8 x 2^22 paths, level kernel + merge each
         lin = arv.load_table("dyadic_linear_k15")
         sps = [arv.LevelSpec(level=lv, scheme="euler_maruyama", process=arv.GbmParams(0.05, 0.2, 1.0, 1.0),
