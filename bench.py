@@ -691,7 +691,8 @@ def mlmc_metrics(arv, args, rank, world, device) -> dict:
         entry = {"paths_per_level": n_paths, "levels": [levels[0], levels[-1]], "seconds": secs,
                  "paths_per_s": paths_total / secs, "path_steps_per_s": n_paths * steps / secs,
                  "api": "estimate_level_suites (all levels back to back, one host sync)" +
-                        (f"; one NCCL all-reduce pair of all levels' triples over {world} ranks" if world > 1 else "")}
+                        (f"; one {dist.get_backend().upper()} all-reduce pair of all levels' triples over {world} ranks"
+                         if world > 1 else "")}
         entry["roofline"] = _fp64_roofline("gbm_level8" if scheme != "cir_exact" else "cir_level6",
                                            n_paths * steps / secs)
         if scheme == "cir_exact":

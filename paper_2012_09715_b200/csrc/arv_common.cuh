@@ -6,10 +6,25 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cassert>
 #include <cstdio>
 #include <string>
 
 #include "approxrv_b200.h"
+
+// Device-side bounds / invariant checks for the checked build
+// (-DARV_CHECKS=1, tools/build_checked.py): compute-sanitizer is closed on the
+// GPU pool, so the risky indices (warp tail lists, CIR bucket scatter, table
+// indices, finalize tickets) assert their ranges instead and the GPU test
+// suite runs against that library.  Compiled out otherwise.
+#ifndef ARV_CHECKS
+#define ARV_CHECKS 0
+#endif
+#if ARV_CHECKS
+#define ARV_DCHECK(c) assert(c)
+#else
+#define ARV_DCHECK(c) ((void)0)
+#endif
 
 namespace arv {
 

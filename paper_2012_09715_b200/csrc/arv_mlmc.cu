@@ -359,7 +359,11 @@ __global__ void __launch_bounds__(kFinStageBlock) k_finalize_chunks(const double
     if (threadIdx.x < NK * 3) fs->stage[blockIdx.x][threadIdx.x / 3][threadIdx.x % 3] = r[threadIdx.x / 3][threadIdx.x % 3];
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(&fs->ticket, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) {
+        const unsigned t = atomicAdd(&fs->ticket, 1u);
+        ARV_DCHECK(t < gridDim.x);  // the ticket starts at 0 for every call
+        last = t == gridDim.x - 1;
+    }
     __syncthreads();
     if (!last) return;
     __threadfence();
@@ -569,7 +573,10 @@ __device__ __forceinline__ void as241_words(const uint32_t (&w)[N], const double
     if (total) {  // warp-uniform
 #pragma unroll
         for (int k = 0; k < N; ++k)
-            if ((pend >> k) & 1u) buf[pos[k]] = v[k];
+            if ((pend >> k) & 1u) {
+                ARV_DCHECK(pos[k] >= 0 && pos[k] < total && total <= 32 * N);
+                buf[pos[k]] = v[k];
+            }
         __syncwarp();
         for (int g = threadIdx.x & 31; g < total; g += 32) buf[g] = tail_abs<FMA>(buf[g]);
         __syncwarp();
@@ -598,12 +605,14 @@ __device__ __forceinline__ double table(const double *sm, uint32_t w, double v, 
         const double u = __dsub_rn(one_plus_u32(w), 1.0);
         long long idx = static_cast<long long>(__dmul_rn(static_cast<double>(K1), u));
         idx = idx < K1 ? idx : K1 - 1;
+        ARV_DCHECK(idx >= 0 && idx < K1);
         return sm[idx];
     } else {
         constexpr int S = (DEG + 2) & ~1;
         const uint32_t neg = static_cast<uint32_t>(static_cast<int32_t>(w) >> 31);
         int idx = __clz(w ^ neg);  // 1022 - expo(v), _kernels.pyx:36
         idx = idx < cap ? idx : cap;
+        ARV_DCHECK(idx >= 0 && idx <= cap);
         const double *c = sm + idx * S;
         double z;
         if constexpr (DEG == 1) {
@@ -931,6 +940,7 @@ __global__ void __launch_bounds__(kCirBlock, ARV_CIR_MINB) k_cir_exact_level(Lev
             G.pid_out[i] = pid;
             const uint32_t b = cir_bucket(__dmul_rn(x_e, A.decay_over_scale));
             G.bucket[i] = b;
+            ARV_DCHECK(b < kCirBuckets);
             atomicAdd(&hist[b], 1u);
         }
         __syncthreads();
@@ -1009,6 +1019,7 @@ __global__ void __launch_bounds__(kCirBlock) k_cir_scatter(int64_t n, const uint
     __syncthreads();
     if (i < n) {
         const uint32_t dst = base[b] + local;
+        ARV_DCHECK(b < kCirBuckets && dst < static_cast<uint64_t>(n));
         xe_o[dst] = xe[i];
         xa_o[dst] = xa[i];
         rs_o[dst] = rs[i];
