@@ -496,6 +496,12 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
 #ifndef ARV_GBM_V2_MINB
 #define ARV_GBM_V2_MINB 4
 #endif
+#ifndef ARV_GBM_DIV_CORRECT  // residual-corrected (correctly rounded) division on the exact side
+#define ARV_GBM_DIV_CORRECT 0  // 0: n * rcp(d) (~1 ulp): config 4 11.74 -> 11.15 ms with FMA steps
+#endif
+#ifndef ARV_GBM_FMA_STEP  // exact-side GBM steps as FMAs
+#define ARV_GBM_FMA_STEP 1
+#endif
 
 namespace g2 {
 // coefficient sets: rows of the __constant__ table kAS241d (A, B, C, D, E, F);
@@ -527,8 +533,12 @@ __device__ __forceinline__ double divide(double n, double d) {
         asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
         y = fma(fma(-d, y, 1.0), y, y);
         y = fma(fma(-d, y, 1.0), y, y);
+#if ARV_GBM_DIV_CORRECT
         const double q0 = __dmul_rn(n, y);
         return fma(fma(-d, q0, n), y, q0);
+#else
+        return __dmul_rn(n, y);  // within ~1 ulp of n / d (the residual correction costs two DFMA)
+#endif
     }
 }
 
@@ -709,9 +719,21 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
             return cir_step<MIL>(x, dw, dt, A.a, A.b, A.c);
         }
     };
+    // exact side with ARV_GBM_FMA_STEP: the same GBM step as fused multiply-adds
+    // (x + x (mu dt + sg dw)), one rounding fewer per operation; the approximate
+    // side always keeps the reference's separately rounded em_step
+    auto step_e = [&](double x, double dw, double dt, double mudt) -> double {
+        if constexpr (GBM && FMA && ARV_GBM_FMA_STEP) {
+            double incr = fma(sg, dw, mudt);
+            if (MIL) incr = fma(hs2, fma(dw, dw, -dt), incr);
+            return fma(x, incr, x);
+        } else {
+            return step(x, dw, dt, mudt);
+        }
+    };
     auto pair_step = [&](double z0, double z1, double w0, double w1) {
-        xf_e = step(step(xf_e, __dmul_rn(sq_f, z0), dt_f, mudt_f), __dmul_rn(sq_f, z1), dt_f, mudt_f);
-        xc_e = step(xc_e, __dmul_rn(sq_f, __dadd_rn(z0, z1)), dt_c, mudt_c);
+        xf_e = step_e(step_e(xf_e, __dmul_rn(sq_f, z0), dt_f, mudt_f), __dmul_rn(sq_f, z1), dt_f, mudt_f);
+        xc_e = step_e(xc_e, __dmul_rn(sq_f, __dadd_rn(z0, z1)), dt_c, mudt_c);
         xf_a = step(step(xf_a, __dmul_rn(sq_f, w0), dt_f, mudt_f), __dmul_rn(sq_f, w1), dt_f, mudt_f);
         xc_a = step(xc_a, __dmul_rn(sq_f, __dadd_rn(w0, w1)), dt_c, mudt_c);
     };
@@ -754,7 +776,7 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
         uint32_t w[1] = {draw()};
         double v[1] = {g2::reflected(w[0])}, z[1] = {0.0};
         if (we) g2::as241_words<1, FMA>(w, v, z, buf);
-        if (we) xf_e = step(xf_e, __dmul_rn(sq_f, z[0]), dt_f, mudt_f);
+        if (we) xf_e = step_e(xf_e, __dmul_rn(sq_f, z[0]), dt_f, mudt_f);
         if (wa) xf_a = step(xf_a, __dmul_rn(sq_f, g2::table<DEG>(smd, w[0], v[0], cap, K1)), dt_f, mudt_f);
     }
     double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
