@@ -109,6 +109,29 @@ class TestValidationBeforeCuda:
             nat.call("arv_mlmc_gaussian_level", ctypes.byref(s), None, 1, 16, None, None, None, 0, None)
         parts = (1 << 22) // 256 * 15 * 8
         assert nat.lib.arv_mlmc_workspace_bytes(1 << 22) >= parts  # + chunked-finalize scratch
+        s.sides = 7
+        with pytest.raises(errors.ConfigError, match="sides"):
+            nat.call("arv_mlmc_gaussian_level", ctypes.byref(s), None, 1, 16, None, None, None, 1 << 30, None)
+
+    def test_host_buffer_entry_points_validate_first(self, nat):
+        """arv_host_* (host numpy buffers) reject bad lengths / pointers and treat
+        n = 0 as a no-op before touching CUDA (no pipeline is created)."""
+        from paper_2012_09715_b200 import errors
+
+        u = np.zeros(4)
+        with pytest.raises(errors.ConfigError, match="negative length"):
+            nat.call("arv_host_dyadic_eval", None, 1, 16, u.ctypes.data, u.ctypes.data, -1, None)
+        with pytest.raises(errors.ConfigError, match="null host pointer"):
+            nat.call("arv_host_dyadic_eval", None, 1, 16, None, u.ctypes.data, 4, None)
+        with pytest.raises(errors.ConfigError, match="1 or n elements"):
+            nat.call("arv_host_ncchi2_eval", None, 64, 1, 16, 2.0, u.ctypes.data, u.ctypes.data, 3, u.ctypes.data,
+                     4, None)
+        for name, args in (("arv_host_dyadic_eval32", (None, 1, 16, None, None, 0, None)),
+                           ("arv_host_constant_eval", (None, 1024, None, None, 0, None)),
+                           ("arv_host_dyadic_index", (None, 0, 15, None, None)),
+                           ("arv_host_gaussian_inv_cdf", (None, None, 0, None))):
+            nat.call(name, *args)
+        assert nat.launch_count() == 0
 
 
 class TestHostMirror:
