@@ -37,6 +37,10 @@ namespace arv {
 #define ARV_GEN_UNROLL 2
 #endif
 constexpr int kGenUnroll = ARV_GEN_UNROLL;
+#ifndef ARV_SIGNED_UNROLL
+#define ARV_SIGNED_UNROLL 1
+#endif
+constexpr int kSignedUnroll = ARV_SIGNED_UNROLL;  // the signed-table generator (headline)
 // Process-wide launch shape knobs (arv_set_tuning); defaults from sweeps.
 static int g_group = 8;        // samples per thread-group: 4 (v4) or 8 (v8)
 static int g_ctas_per_sm = 0;  // CTAs per SM (256 threads each); 0 = auto (see gen_grid)
@@ -137,7 +141,7 @@ __device__ __forceinline__ void eval_two(const Eval &eval, uint32_t w0, uint32_t
 
 // The group loop: thread g0 starts at state `s` (its first group) and
 // produces its groups with G-wide stores (out must be 4*G-byte aligned).
-template <int G, class Eval>
+template <int G, int U = kGenUnroll, class Eval>
 __device__ __forceinline__ void gen_run(const GenArgs &a, uint32_t *__restrict__ out, const Eval &eval, uint64_t s,
                                         uint64_t g0) {
     const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -151,7 +155,7 @@ __device__ __forceinline__ void gen_run(const GenArgs &a, uint32_t *__restrict__
     const uint32_t iters = static_cast<uint32_t>(a.iter_q) + (g0 < a.iter_r ? 1u : 0u);
     uint32_t *p = out + G * g0;
     const uint64_t step = G * T;
-#pragma unroll kGenUnroll
+#pragma unroll U
     for (uint32_t it = 0; it < iters; ++it) {
         uint32_t w[G];
 #pragma unroll
@@ -515,7 +519,10 @@ __global__ void __launch_bounds__(256, ARV_GEN_MINB) k_pcg32_linsigned(GenArgs a
     float2 *tab = reinterpret_cast<float2 *>(smem4);
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
     if (stage_linsigned(tab, coeffs, K, b)) {
-        gen_run<MODE>(a, out, EvalLinSigned{sbase - 8u * (kSignedE0 << b), 23 - b, 8u + threadIdx.x * a.zero32}, s, g0);
+        // not unrolled: 182.0 vs 184.7 us (unroll 2) / 188.9 us (unroll 4) at 2^28,
+        // sustained 210.3 vs 211.3 / 216.4 us (tools/gen_tune.py)
+        gen_run<MODE, kSignedUnroll>(a, out, EvalLinSigned{sbase - 8u * (kSignedE0 << b), 23 - b,
+                                                           8u + threadIdx.x * a.zero32}, s, g0);
     } else {  // CTA-uniform
         float *sm = reinterpret_cast<float *>(smem4);
         __syncthreads();

@@ -66,6 +66,27 @@ def main():
         ms = best_ms(lambda: arv.Pcg32Stream(42, 0).sample_exact64(n, out=out64[:n]), args.reps)
         row["as241_f64"] = {"samples_per_s": n / ms * 1e3, "ms": ms}
         print(json.dumps(row), flush=True)
+    print(json.dumps({"accuracy": accuracy(tabs)}), flush=True)
+
+
+def accuracy(tabs, n=1 << 24):
+    """Errors against AS241 in f64 on the same f32 lattice uniforms (the fused
+    generators' inputs): the f32 AS241 evaluation (max relative error and f32
+    ulps) and each table approximation (RMSE, max |error|)."""
+    from paper_2012_09715_b200 import _kernels
+
+    u = arv.Pcg32Stream(42, 0).uniforms(n)                      # f32 lattice
+    ref = torch.empty(n, dtype=torch.float64, device="cuda")
+    _kernels.gaussian_inv_cdf(u.double(), ref)                  # AS241 f64 of the same u
+    z32 = arv.Pcg32Stream(42, 0).sample("exact", n)             # AS241 in f32 (fused)
+    d = z32.double() - ref
+    rel = (d.abs() / ref.abs().clamp_min(1e-300)).max().item()
+    ulp = (d.abs() / (torch.nextafter(z32.abs(), torch.tensor(float("inf"), device="cuda")) - z32.abs()).double()).max().item()
+    res = {"samples": n, "as241_f32_vs_f64": {"max_rel": rel, "max_abs": d.abs().max().item(), "max_f32_ulp": ulp}}
+    for name, t in tabs.items():
+        e = arv.Pcg32Stream(42, 0).sample(t, n).double() - ref
+        res[name] = {"rmse": torch.sqrt((e * e).mean()).item(), "max_abs": e.abs().max().item()}
+    return res
 
 
 if __name__ == "__main__":
