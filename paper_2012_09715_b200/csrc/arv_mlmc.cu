@@ -499,6 +499,9 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
 #ifndef ARV_GBM_DIV_CORRECT  // residual-corrected (correctly rounded) division on the exact side
 #define ARV_GBM_DIV_CORRECT 0  // 0: n * rcp(d) (~1 ulp): config 4 11.74 -> 11.15 ms with FMA steps
 #endif
+#ifndef ARV_GBM_LOCKSTEP  // central rationals of the N words in lockstep
+#define ARV_GBM_LOCKSTEP 1  // 11.14 -> 11.06 ms (config 4)
+#endif
 #ifndef ARV_GBM_FMA_STEP  // exact-side GBM steps as FMAs
 #define ARV_GBM_FMA_STEP 1
 #endif
@@ -566,10 +569,34 @@ template <int N, bool FMA>
 __device__ __forceinline__ void as241_words(const uint32_t (&w)[N], const double (&v)[N], double (&z)[N],
                                             double *buf) {
     unsigned pend = 0;
+#if ARV_GBM_LOCKSTEP
+    if constexpr (FMA) {  // the N central rationals in lockstep: 2N independent Horner chains
+        double q[N], r[N], a[N], b[N];
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-        if (w[k] - kCentralLo > kCentralSpan) pend |= 1u << k;
-        z[k] = central<FMA>(__dsub_rn(one_plus_u32(w[k]), 1.5));  // q = u - 1/2 exactly
+        for (int k = 0; k < N; ++k) {
+            if (w[k] - kCentralLo > kCentralSpan) pend |= 1u << k;
+            q[k] = __dsub_rn(one_plus_u32(w[k]), 1.5);
+            r[k] = fma(-q[k], q[k], 0.180625);
+            a[k] = kAS241d[kA][7];
+            b[k] = kAS241d[kB][7];
+        }
+#pragma unroll
+        for (int i = 6; i >= 0; --i)
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                a[k] = fma(a[k], r[k], kAS241d[kA][i]);
+                b[k] = fma(b[k], r[k], kAS241d[kB][i]);
+            }
+#pragma unroll
+        for (int k = 0; k < N; ++k) z[k] = divide<FMA>(__dmul_rn(q[k], a[k]), b[k]);
+    } else
+#endif
+    {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            if (w[k] - kCentralLo > kCentralSpan) pend |= 1u << k;
+            z[k] = central<FMA>(__dsub_rn(one_plus_u32(w[k]), 1.5));  // q = u - 1/2 exactly
+        }
     }
     const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
     int pos[N];
