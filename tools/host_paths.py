@@ -99,6 +99,40 @@ def suites():
     print(s.getvalue()[-3500:])
 
 
+def graph():
+    """Per-call cost of small fused-generator requests: eager calls (Python +
+    ctypes + launch each) vs the same calls replayed from one CUDA graph."""
+    import paper_2012_09715_b200 as arv
+
+    sub = arv.load_table("subdyadic_linear_k16_s8")
+    for lg in (16, 20, 24):
+        n, k = 1 << lg, 64
+        out = torch.empty((k, n), dtype=torch.float32, device="cuda")
+        s = arv.Pcg32Stream(42, 0)
+        for i in range(k):
+            s.sample(sub, n, out=out[i])
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(5):
+            for i in range(k):
+                s.sample(sub, n, out=out[i])
+        torch.cuda.synchronize()
+        eager = (time.perf_counter() - t) / (5 * k)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(k):
+                s.sample(sub, n, out=out[i])
+        g.replay()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(5):
+            g.replay()
+        torch.cuda.synchronize()
+        replay = (time.perf_counter() - t) / (5 * k)
+        print(f"2^{lg} samples per call: eager {eager * 1e6:.2f} us/call, graph replay {replay * 1e6:.2f} us/call "
+              f"({n / replay:.3e} samples/s)", flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     if what == "all":
@@ -106,5 +140,6 @@ if __name__ == "__main__":
         for th in ("8", "16"):
             subprocess.run([sys.executable, __file__, "plugin"], env=dict(os.environ, ARV_HOST_THREADS=th))
         suites()
+        graph()
     else:
         globals()[what]()
