@@ -499,6 +499,9 @@ __global__ void __launch_bounds__(kLevelBlock, (SCHEME == ARV_SCHEME_EM || SCHEM
 #ifndef ARV_GBM_DIV_CORRECT  // residual-corrected (correctly rounded) division on the exact side
 #define ARV_GBM_DIV_CORRECT 0  // 0: n * rcp(d) (~1 ulp): config 4 11.74 -> 11.15 ms with FMA steps
 #endif
+#ifndef ARV_GBM_SIDES_SPLIT  // a both-sides instantiation without the per-iteration side tests
+#define ARV_GBM_SIDES_SPLIT 1  // 11.06 -> 10.73 ms (config 4)
+#endif
 #ifndef ARV_GBM_LOCKSTEP  // central rationals of the N words in lockstep
 #define ARV_GBM_LOCKSTEP 1  // 11.14 -> 11.06 ms (config 4)
 #endif
@@ -666,7 +669,7 @@ __device__ __forceinline__ double table(const double *sm, uint32_t w, double v, 
 }
 }  // namespace g2
 
-template <int DEG, int SCHEME>
+template <int DEG, int SCHEME, bool BOTH>
 __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level_v2(LevelArgs A,
                                                                                  const double *__restrict__ coeffs,
                                                                                  int64_t K1,
@@ -735,7 +738,9 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
     const double x0 = A.x0, dt_f = A.dt_f, dt_c = A.dt_c, sq_f = A.sq_f;
     const double mudt_f = __dmul_rn(A.a, dt_f), mudt_c = __dmul_rn(A.a, dt_c);  // mlmc.py:195
     const double sg = A.b, hs2 = __dmul_rn(__dmul_rn(0.5, A.b), A.b);           // mlmc.py:196-197
-    const bool we = A.want_exact, wa = A.want_approx;
+    // BOTH (sides = both, the MLMC estimators): the side tests are compile-time
+    // true, so the loop body is one basic block the scheduler can interleave
+    const bool we = BOTH || A.want_exact, wa = BOTH || A.want_approx;
     double xf_e = x0, xc_e = x0, xf_a = x0, xc_a = x0;
     auto step = [&](double x, double dw, double dt, double mudt) -> double {
         if constexpr (GBM) {
@@ -1304,8 +1309,11 @@ int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, in
 #define ARV_LAUNCH(D, S)                                                                              \
     (A.rng == ARV_RNG_PHILOX                                                                          \
          ? k_gaussian_level<D, S, true><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths) \
-         : (ARV_GBM_V2 ? k_gaussian_level_v2<D, S><<<grid_v2((const void *)k_gaussian_level_v2<D, S>, nb, smem2), \
-                                                      kLevelBlock, smem2, s>>>(A, coeffs, K1, parts, paths)             \
+         : (ARV_GBM_V2 ? ((A.want_exact && A.want_approx && ARV_GBM_SIDES_SPLIT)                         \
+                              ? k_gaussian_level_v2<D, S, true><<<grid_v2((const void *)k_gaussian_level_v2<D, S, true>, nb, smem2), \
+                                                                  kLevelBlock, smem2, s>>>(A, coeffs, K1, parts, paths) \
+                              : k_gaussian_level_v2<D, S, false><<<grid_v2((const void *)k_gaussian_level_v2<D, S, false>, nb, smem2), \
+                                                                   kLevelBlock, smem2, s>>>(A, coeffs, K1, parts, paths)) \
                        : k_gaussian_level<D, S, false><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths)))
 #define ARV_SCHEMES(D)                                                                      \
     case D:                                                                                 \
