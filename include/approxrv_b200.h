@@ -170,6 +170,10 @@ ARV_API int arv_store_probe_ex(float *out, int64_t n, int mode, void *stream);
 /* ARV_TUNE_CIR_SEGMENT = steps per segment of a CIR exact level (default 4;
  * 0 = one kernel per level); see arv_mlmc_cir_workspace_bytes. */
 #define ARV_TUNE_CIR_SEGMENT 3
+/* ARV_TUNE_GBM_KERNEL = Gaussian level kernel for both-sides PCG32 levels:
+ * 0 (default), 2 (per-iteration warp tail lists) or 3 (phased tail list);
+ * both give bit-identical paths and statistics. */
+#define ARV_TUNE_GBM_KERNEL 4
 ARV_API int arv_set_tuning(int key, int value);
 
 /* ---- nested MLMC level kernels ------------------------------------------

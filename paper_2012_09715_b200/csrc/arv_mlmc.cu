@@ -17,6 +17,10 @@
 // n_paths_total per step with a single precomputed affine map, i.e. one
 // 64-bit multiply-add per step, as in a plain LCG.
 #include <cmath>
+#include <mutex>
+#include <type_traits>
+#include <utility>
+#include <vector>
 
 #include "arv_common.cuh"
 #include "arv_eval_dev.cuh"
@@ -566,11 +570,10 @@ __device__ __forceinline__ double tail_abs(double w) {
     return divide<FMA>(horner<FMA>(kE, x), horner<FMA>(kF, x));
 }
 
-// AS241 of N words per lane; all 32 lanes of the warp call it together.
-// v[k] = min(u, 1 - u) of element k (exact).  buf: this warp's 32 N doubles.
+// Central rational of N words (every element; tail elements get a value
+// that the caller replaces) and the tail bits (|u - 1/2| > 0.425).
 template <int N, bool FMA>
-__device__ __forceinline__ void as241_words(const uint32_t (&w)[N], const double (&v)[N], double (&z)[N],
-                                            double *buf) {
+__device__ __forceinline__ unsigned central_words(const uint32_t (&w)[N], double (&z)[N]) {
     unsigned pend = 0;
 #if ARV_GBM_LOCKSTEP
     if constexpr (FMA) {  // the N central rationals in lockstep: 2N independent Horner chains
@@ -601,6 +604,15 @@ __device__ __forceinline__ void as241_words(const uint32_t (&w)[N], const double
             z[k] = central<FMA>(__dsub_rn(one_plus_u32(w[k]), 1.5));  // q = u - 1/2 exactly
         }
     }
+    return pend;
+}
+
+// AS241 of N words per lane; all 32 lanes of the warp call it together.
+// v[k] = min(u, 1 - u) of element k (exact).  buf: this warp's 32 N doubles.
+template <int N, bool FMA>
+__device__ __forceinline__ void as241_words(const uint32_t (&w)[N], const double (&v)[N], double (&z)[N],
+                                            double *buf) {
+    const unsigned pend = central_words<N, FMA>(w, z);
     const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
     int pos[N];
     int total = 0;
@@ -831,6 +843,221 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
         }
     }
     cta_moments<ARV_NKIND>(d, valid, parts + tile * 3 * ARV_NKIND);
+    }
+}
+
+// ------------------------------------------ Gaussian level kernel, v3 --
+// Both sides, PCG32 (the MLMC estimators' case).  Same paths, bit for bit, as
+// k_gaussian_level_v2 (same functions per element, same tile partition of the
+// statistics); the exact side is reorganised in phases over blocks of
+// kV3Steps uniforms of the CTA's 256 paths:
+//   1. every thread draws its block's words; evaluates the central rational of
+//      each in lockstep groups of 4 (the A/B coefficients stay in uniform
+//      registers for the whole phase) and stores z -- or, for a tail element,
+//      +-v (v = min(u, 1 - u), the sign marking the upper tail) -- in zbuf,
+//      its tail slots going to one CTA-wide list (one atomic per warp); and
+//      runs the whole approximate side (table, both approximate path
+//      updates), which needs nothing from the exact side;
+//   2. the CTA's 256 threads serve the whole list: log, sqrt, C/D (E/F)
+//      rational per entry -- ~450 tails per 12-step block, ~80% of the lanes
+//      busy instead of ~60% with the per-iteration warp lists, and the tail
+//      constants loaded once per pass instead of once per four uniforms;
+//   3. every thread reads its z back and advances the two exact-side paths.
+// Each thread only touches its own column of zbuf in phases 1 and 3, so two
+// barriers per block suffice (after 1 and after 2).  Shared memory per block:
+// 10 B per element (z and a 16-bit list slot).
+#ifndef ARV_GBM_V3
+#define ARV_GBM_V3 1
+#endif
+#ifndef ARV_V3_STEPS
+#define ARV_V3_STEPS 20  // config 4: 12 -> 10.26 ms, 16 -> 9.95, 20 -> 9.89, 24 -> 10.02 (3 CTAs/SM)
+#endif
+constexpr int kV3Steps = ARV_V3_STEPS;
+static_assert(kV3Steps % 2 == 0 && kV3Steps <= 32 && kV3Steps * kLevelBlock <= 65536,
+              "block of uniforms (32-bit tail mask, u16 tail slots)");
+
+__host__ __device__ constexpr int64_t v3_table_words(int degree, int64_t K1) {
+    return ((degree == 0 ? K1 : static_cast<int64_t>((degree + 2) & ~1) * K1) + 1) & ~int64_t(1);
+}
+__host__ __device__ constexpr size_t v3_smem_bytes(int degree, int64_t K1) {
+    return sizeof(double) * v3_table_words(degree, K1) +
+           static_cast<size_t>(kV3Steps) * kLevelBlock * (sizeof(double) + sizeof(uint16_t));
+}
+
+template <int DEG, int SCHEME>
+__global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level_v3(LevelArgs A,
+                                                                                 const double *__restrict__ coeffs,
+                                                                                 int64_t K1,
+                                                                                 double *__restrict__ parts,
+                                                                                 double *__restrict__ paths) {
+    constexpr bool FMA = ARV_GBM_FMA_EXACT != 0;
+    constexpr bool GBM = SCHEME == ARV_SCHEME_EM || SCHEME == ARV_SCHEME_MILSTEIN;
+    constexpr bool MIL = SCHEME == ARV_SCHEME_MILSTEIN || SCHEME == ARV_SCHEME_CIR_MILSTEIN_TRUNCATED;
+    constexpr int S = DEG == 0 ? 1 : (DEG + 2) & ~1;
+    constexpr int NB = kLevelBlock;
+    extern __shared__ __align__(16) double smd[];
+    double *zbuf = smd + v3_table_words(DEG, K1);                         // [kV3Steps][NB]
+    uint16_t *list = reinterpret_cast<uint16_t *>(zbuf + kV3Steps * NB);  // tail slots k * NB + t
+    __shared__ int tail_cnt[2];
+    if constexpr (DEG == 0) {
+        for (int i = threadIdx.x; i < K1; i += blockDim.x) smd[i] = __ldg(coeffs + i);
+    } else {
+        for (int i = threadIdx.x; i < (DEG + 1) * K1; i += blockDim.x) {
+            const int d = static_cast<int>(i / K1), j = static_cast<int>(i % K1);
+            smd[j * S + d] = __ldg(coeffs + i);
+        }
+    }
+    if (threadIdx.x < 2) tail_cnt[threadIdx.x] = 0;
+    const int cap = static_cast<int>(K1 - 1);
+    const int t = threadIdx.x, lane = t & 31;
+    __shared__ Affine lane_map[NB + 1];  // as k_gaussian_level_v2
+    {
+        Affine m{1, 0};
+        for (int b = 0; b < 8; ++b)
+            if ((static_cast<unsigned>(t) >> b) & 1u) m = {A.jump2[b].a * m.a, A.jump2[b].a * m.c + A.jump2[b].c};
+        lane_map[t] = m;
+        if (t == 0) {
+            Affine g{1, 0};
+            const uint64_t stride = static_cast<uint64_t>(gridDim.x) * NB;
+            for (int b = 0; b < kPathJumpBits; ++b)
+                if ((stride >> b) & 1u) g = {A.jump2[b].a * g.a, A.jump2[b].a * g.c + A.jump2[b].c};
+            lane_map[NB] = g;
+        }
+    }
+    const int64_t ntiles = (A.path_count + NB - 1) / NB;
+    uint64_t tile_s = path_start_state(A, static_cast<uint64_t>(A.path_lo) + static_cast<uint64_t>(blockIdx.x) * NB);
+    __syncthreads();
+    unsigned blk = 0;  // running block index: selects the tail counter
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t i = tile * NB + t;
+        const bool valid = i < A.path_count;
+        uint64_t s;
+        {
+            const Affine my = lane_map[t], nx = lane_map[NB];
+            s = my.a * tile_s + my.c;
+            tile_s = nx.a * tile_s + nx.c;
+        }
+        const Affine st = A.step;
+        const double x0 = A.x0, dt_f = A.dt_f, dt_c = A.dt_c, sq_f = A.sq_f;
+        const double mudt_f = __dmul_rn(A.a, dt_f), mudt_c = __dmul_rn(A.a, dt_c);  // mlmc.py:195
+        const double sg = A.b, hs2 = __dmul_rn(__dmul_rn(0.5, A.b), A.b);           // mlmc.py:196-197
+        double xf_e = x0, xc_e = x0, xf_a = x0, xc_a = x0;
+        auto step = [&](double x, double dw, double dt, double mudt) -> double {
+            if constexpr (GBM) {
+                double incr = __dadd_rn(mudt, __dmul_rn(sg, dw));
+                if (MIL) incr = __dadd_rn(incr, __dmul_rn(hs2, __dsub_rn(__dmul_rn(dw, dw), dt)));
+                return __dmul_rn(x, __dadd_rn(1.0, incr));
+            } else {
+                return cir_step<MIL>(x, dw, dt, A.a, A.b, A.c);
+            }
+        };
+        auto step_e = [&](double x, double dw, double dt, double mudt) -> double {
+            if constexpr (GBM && FMA && ARV_GBM_FMA_STEP) {
+                double incr = fma(sg, dw, mudt);
+                if (MIL) incr = fma(hs2, fma(dw, dw, -dt), incr);
+                return fma(x, incr, x);
+            } else {
+                return step(x, dw, dt, mudt);
+            }
+        };
+        auto draw = [&]() -> uint32_t {
+            const uint32_t w = pcg32_output(s);
+            s = st.a * s + st.c;
+            return w;
+        };
+        // phase 1 for N consecutive elements k0 .. k0 + N - 1 (k0 even; N = 4, 2,
+        // or 1 for the single last step of an odd fine-step count)
+        auto phase1 = [&](auto nconst, int k0, unsigned &pend) {
+            constexpr int N = decltype(nconst)::value;
+            uint32_t w[N];
+            double z[N], a[N];
+#pragma unroll
+            for (int k = 0; k < N; ++k) w[k] = draw();
+            const unsigned pb = g2::central_words<N, FMA>(w, z);
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                const double v = g2::reflected(w[k]);
+                // a tail element parks +-v: the sign marks the upper tail
+                zbuf[(k0 + k) * NB + t] = (pb >> k) & 1u ? (w[k] >> 31 ? v : -v) : z[k];
+                a[k] = g2::table<DEG>(smd, w[k], v, cap, K1);
+            }
+            pend |= pb << k0;
+#pragma unroll
+            for (int k = 0; k + 1 < N; k += 2) {  // the approximate side (mlmc.py:216-220)
+                xf_a = step(step(xf_a, __dmul_rn(sq_f, a[k]), dt_f, mudt_f), __dmul_rn(sq_f, a[k + 1]), dt_f, mudt_f);
+                xc_a = step(xc_a, __dmul_rn(sq_f, __dadd_rn(a[k], a[k + 1])), dt_c, mudt_c);
+            }
+            if constexpr (N == 1) xf_a = step(xf_a, __dmul_rn(sq_f, a[0]), dt_f, mudt_f);  // mlmc.py:221-226
+        };
+        for (int64_t k_lo = 0; k_lo < A.n_f; k_lo += kV3Steps) {
+            const int L = static_cast<int>(A.n_f - k_lo < kV3Steps ? A.n_f - k_lo : kV3Steps);
+            // ---- phase 1
+            unsigned pend = 0;
+            int k0 = 0;
+            for (; k0 + 4 <= L; k0 += 4) phase1(std::integral_constant<int, 4>{}, k0, pend);
+            if (k0 + 2 <= L) {
+                phase1(std::integral_constant<int, 2>{}, k0, pend);
+                k0 += 2;
+            }
+            if (k0 < L) phase1(std::integral_constant<int, 1>{}, k0, pend);
+            {  // append this thread's tail slots to the CTA list
+                const int np = __popc(pend);
+                int incl = np;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                int base = 0;
+                if (lane == 31 && incl) base = atomicAdd(&tail_cnt[blk & 1u], incl);
+                base = __shfl_sync(0xffffffffu, base, 31);
+                int pos = base + incl - np;
+                for (unsigned m = pend; m; m &= m - 1u) {
+                    ARV_DCHECK(pos < kV3Steps * NB);
+                    list[pos++] = static_cast<uint16_t>((__ffs(m) - 1) * NB + t);
+                }
+            }
+            __syncthreads();
+            // ---- phase 2: the CTA serves the whole tail list
+            {
+                const int nt = tail_cnt[blk & 1u];
+                if (t == 0) tail_cnt[(blk + 1u) & 1u] = 0;  // the next block's counter (idle since the last barrier)
+                for (int q = t; q < nt; q += NB) {
+                    const int slot = list[q];
+                    const double pv = zbuf[slot];
+                    zbuf[slot] = copysign(g2::tail_abs<FMA>(fabs(pv)), pv);  // upper tail positive (exact_dist.py:124-126)
+                }
+            }
+            __syncthreads();
+            // ---- phase 3: the exact-side paths, in step order
+            int k = 0;
+            for (; k + 2 <= L; k += 2) {
+                const double z0 = zbuf[k * NB + t], z1 = zbuf[(k + 1) * NB + t];
+                xf_e = step_e(step_e(xf_e, __dmul_rn(sq_f, z0), dt_f, mudt_f), __dmul_rn(sq_f, z1), dt_f, mudt_f);
+                xc_e = step_e(xc_e, __dmul_rn(sq_f, __dadd_rn(z0, z1)), dt_c, mudt_c);
+            }
+            if (k < L) xf_e = step_e(xf_e, __dmul_rn(sq_f, zbuf[k * NB + t]), dt_f, mudt_f);
+            ++blk;
+        }
+        double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        if (valid) {
+            const double fe = payoff_fn(xf_e, A.payoff, A.strike);
+            const double fa = payoff_fn(xf_a, A.payoff, A.strike);
+            const double ce = A.level > 0 ? payoff_fn(xc_e, A.payoff, A.strike) : 0.0;
+            const double ca = A.level > 0 ? payoff_fn(xc_a, A.payoff, A.strike) : 0.0;
+            d[0] = __dsub_rn(fe, ce);
+            d[1] = __dsub_rn(fa, ca);
+            d[2] = __dadd_rn(__dsub_rn(__dsub_rn(fe, ce), fa), ca);
+            d[3] = fe;
+            d[4] = fa;
+            if (paths) {
+                paths[i] = fe;
+                paths[A.path_count + i] = ce;
+                paths[2 * A.path_count + i] = fa;
+                paths[3 * A.path_count + i] = ca;
+            }
+        }
+        cta_moments<ARV_NKIND>(d, valid, parts + tile * 3 * ARV_NKIND);
     }
 }
 
@@ -1214,6 +1441,9 @@ static int run_finalize(double *parts, int64_t nb, double *stats, cudaStream_t s
 // Steps per segment of a segmented CIR exact level (0: always one kernel);
 // arv_set_tuning(ARV_TUNE_CIR_SEGMENT).
 int g_cir_segment = 4;
+// Gaussian level kernel for both-sides PCG32 levels: 0 = default, 2 or 3;
+// arv_set_tuning(ARV_TUNE_GBM_KERNEL) (tests compare the two bit for bit).
+int g_gbm_kernel = 0;
 
 static int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
 
@@ -1271,6 +1501,18 @@ int64_t arv_mlmc_cir_workspace_bytes(int64_t path_count) {
     return CirWs(path_count < 1 ? 1 : path_count, nullptr).total;
 }
 
+// Raise a kernel's dynamic shared-memory limit (static + dynamic may pass
+// the 48 KB default) once per kernel and size.
+static void allow_dyn_smem(const void *fn, size_t bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void *, size_t>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto &e : done)
+        if (e.first == fn && e.second >= bytes) return;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    done.emplace_back(fn, bytes);
+}
+
 // one wave of resident CTAs (at most one per tile)
 #ifndef ARV_GBM_V2_WAVES
 #define ARV_GBM_V2_WAVES 8  // waves of the grid: 1 -> 5.97 ms at level 8, 2 -> 5.69, 8 -> 5.55 (dynamic CTA scheduling still pays)
@@ -1305,23 +1547,34 @@ int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, in
     const size_t smem = sizeof(double) * (degree + 1) * K1;
     // v2 table layout: interleaved [K1][S], S = degree + 1 rounded up to even
     const size_t smem2 = sizeof(double) * (degree == 0 ? 1 : ((degree + 2) & ~1)) * K1;
+    // v3 (phased exact side): both sides wanted, PCG32; the table + the block buffers
+    const size_t smem3 = v3_smem_bytes(degree, K1);
+    const int kern = g_gbm_kernel ? g_gbm_kernel : (ARV_GBM_V3 ? 3 : 2);
+    const bool use_v3 = kern == 3 && A.rng == ARV_RNG_PCG32 && A.want_exact && A.want_approx &&
+                        smem3 <= 96 * 1024;
     cudaStream_t s = as_stream(stream);
 #define ARV_LAUNCH(D, S)                                                                              \
     (A.rng == ARV_RNG_PHILOX                                                                          \
          ? k_gaussian_level<D, S, true><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths) \
+         : (use_v3 ? k_gaussian_level_v3<D, S><<<grid_v2((const void *)k_gaussian_level_v3<D, S>, nb, smem3), \
+                                                 kLevelBlock, smem3, s>>>(A, coeffs, K1, parts, paths)                     \
          : (ARV_GBM_V2 ? ((A.want_exact && A.want_approx && ARV_GBM_SIDES_SPLIT)                         \
                               ? k_gaussian_level_v2<D, S, true><<<grid_v2((const void *)k_gaussian_level_v2<D, S, true>, nb, smem2), \
                                                                   kLevelBlock, smem2, s>>>(A, coeffs, K1, parts, paths) \
                               : k_gaussian_level_v2<D, S, false><<<grid_v2((const void *)k_gaussian_level_v2<D, S, false>, nb, smem2), \
                                                                    kLevelBlock, smem2, s>>>(A, coeffs, K1, parts, paths)) \
-                       : k_gaussian_level<D, S, false><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths)))
+                       : k_gaussian_level<D, S, false><<<(unsigned)nb, kLevelBlock, smem, s>>>(A, coeffs, K1, parts, paths))))
+#define ARV_V3_ATTR(D, S) \
+    if (use_v3) allow_dyn_smem((const void *)k_gaussian_level_v3<D, S>, smem3);
 #define ARV_SCHEMES(D)                                                                      \
     case D:                                                                                 \
         switch (scheme) {                                                                   \
-            case ARV_SCHEME_EM: ARV_LAUNCH(D, ARV_SCHEME_EM); break;                        \
-            case ARV_SCHEME_MILSTEIN: ARV_LAUNCH(D, ARV_SCHEME_MILSTEIN); break;            \
-            case ARV_SCHEME_CIR_EULER_TRUNCATED: ARV_LAUNCH(D, ARV_SCHEME_CIR_EULER_TRUNCATED); break; \
-            default: ARV_LAUNCH(D, ARV_SCHEME_CIR_MILSTEIN_TRUNCATED); break;               \
+            case ARV_SCHEME_EM: ARV_V3_ATTR(D, ARV_SCHEME_EM) ARV_LAUNCH(D, ARV_SCHEME_EM); break; \
+            case ARV_SCHEME_MILSTEIN: ARV_V3_ATTR(D, ARV_SCHEME_MILSTEIN) ARV_LAUNCH(D, ARV_SCHEME_MILSTEIN); break; \
+            case ARV_SCHEME_CIR_EULER_TRUNCATED: ARV_V3_ATTR(D, ARV_SCHEME_CIR_EULER_TRUNCATED)             \
+                ARV_LAUNCH(D, ARV_SCHEME_CIR_EULER_TRUNCATED); break;                       \
+            default: ARV_V3_ATTR(D, ARV_SCHEME_CIR_MILSTEIN_TRUNCATED)                      \
+                ARV_LAUNCH(D, ARV_SCHEME_CIR_MILSTEIN_TRUNCATED); break;                    \
         }                                                                                   \
         break;
     switch (degree) {
@@ -1335,6 +1588,7 @@ int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, in
     }
 #undef ARV_SCHEMES
 #undef ARV_LAUNCH
+#undef ARV_V3_ATTR
     note_launch();
     if (int rc = check_launch("arv_mlmc_gaussian_level")) return rc;
     return run_finalize(parts, nb, stats, s, "arv_mlmc_gaussian_level(finalize)",

@@ -45,6 +45,7 @@ constexpr int kSignedUnroll = ARV_SIGNED_UNROLL;  // the signed-table generator 
 static int g_group = 8;        // samples per thread-group: 4 (v4) or 8 (v8)
 static int g_ctas_per_sm = 0;  // CTAs per SM (256 threads each); 0 = auto (see gen_grid)
 extern int g_cir_segment;      // arv_mlmc.cu
+extern int g_gbm_kernel;       // arv_mlmc.cu
 
 constexpr int kJumpBits = 24;  // grid threads < 2^24
 
@@ -724,6 +725,10 @@ int arv_set_tuning(int key, int value) {
         case ARV_TUNE_CIR_SEGMENT:
             if (value < 0) return set_error(ARV_ERR_CONFIG, "cir segment must be >= 0");
             g_cir_segment = value;
+            return ARV_OK;
+        case ARV_TUNE_GBM_KERNEL:
+            if (value != 0 && value != 2 && value != 3) return set_error(ARV_ERR_CONFIG, "gbm kernel must be 0, 2 or 3");
+            g_gbm_kernel = value;
             return ARV_OK;
         case ARV_TUNE_CTAS_PER_SM:
             if (value < 0 || value > 32) return set_error(ARV_ERR_CONFIG, "ctas_per_sm must be in [0 (auto), 32]");

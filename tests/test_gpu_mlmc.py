@@ -506,3 +506,32 @@ def test_estimate_level_suites_equals_per_level_calls(arv):
             assert got[k].cost_per_path_seconds > 0
     with pytest.raises(arv.ConfigError):
         arv.estimate_level_suites(specs, [], n)
+
+
+@pytest.mark.parametrize("scheme,tab,level,n0", [
+    ("euler_maruyama", "dyadic_linear_k15", 0, 1), ("euler_maruyama", "dyadic_linear_k15", 5, 1),
+    ("milstein", "dyadic_cubic_k15", 3, 3), ("euler_maruyama", "constant_q10_l1", 4, 1),
+    ("cir_euler_truncated", "dyadic_linear_k15", 2, 5), ("cir_milstein_truncated", "dyadic_linear_k15", 6, 1),
+    ("euler_maruyama", "dyadic_linear_k15", 0, 7), ("milstein", "dyadic_linear_k15", 4, 3)])
+def test_gaussian_level_kernels_v2_v3_identical(arv, scheme, tab, level, n0):
+    """The phased kernel (v3: CTA-wide tail list over blocks of uniforms) and the
+    per-iteration warp-list kernel (v2) produce the same paths and statistics
+    bit for bit (same per-element functions, same tile partition); n_f odd,
+    blocks shorter than the phase length and ragged path ranges included."""
+    from paper_2012_09715_b200 import _native
+    from paper_2012_09715_b200.mlmc import run_level
+
+    proc = arv.GbmParams(**GBM) if scheme in ("euler_maruyama", "milstein") else arv.CirParams(**CIR)
+    spec = arv.LevelSpec(level=level, scheme=scheme, process=proc, rv_source=arv.load_table(tab),
+                         kind="four_way", n0=n0)
+    out = {}
+    try:
+        for k in (2, 3):
+            _native.call("arv_set_tuning", 4, k)
+            st, paths, _ = run_level(spec, arv.level_stream(42, level, 3), 70001, path_lo=123, path_count=60007,
+                                     want_paths=True)
+            out[k] = (st.cpu().numpy(), paths.cpu().numpy())
+    finally:
+        _native.call("arv_set_tuning", 4, 0)
+    assert np.array_equal(bits(out[2][1]), bits(out[3][1]))
+    assert np.array_equal(bits(out[2][0]), bits(out[3][0]))

@@ -1,4 +1,2 @@
-for r in 1 2; do
-python tools/gen_tune.py
-for lib in tools/ab/*.so; do ARV_LIB_PATH=$lib python tools/gen_tune.py; done
-done
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --tb=short 2>&1 | tail -6
+python tools/prof_kernels.py --which gbmall,gbm --reps 10
