@@ -1,2 +1,3 @@
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --tb=short 2>&1 | tail -3
-bash tools/gpu_ab.sh "--which gbmall,cirall --reps 10" 2>&1 | tail -40 | grep -E "==|all|l0|l6"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gaussian_level -s 2 -c 1 \
+  -o gpurun_out/r2_gbm_l0 python tools/prof_kernels.py --which gbml01 --reps 1 > gpurun_out/r2_ncu_l0.log 2>&1
+tail -1 gpurun_out/r2_ncu_l0.log
