@@ -245,22 +245,7 @@ def _native_spec(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, path_lo: in
     return s
 
 
-def run_level(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, *, path_lo: int = 0,
-              path_count: Optional[int] = None, want_paths: bool = False, device=None, sides: str = "both"):
-    """Launch one level; returns (stats device f64[NSLOT,3], paths or None, n_fail or None).
-
-    The stream's counter is not consulted: paths are addressed from output
-    0 of (seed, stream_id) as in the reference's fresh ``level_stream``.
-    ``sides`` ("both", "exact", "approx") skips the other side's work; its
-    payoffs and statistics slots are then unspecified.
-    """
-    device = device or dev.require_cuda()
-    count = n_paths - path_lo if path_count is None else path_count
-    if n_paths < 1 or count < 1:
-        raise ConfigError("need at least one path")
-    ns = _native_spec(spec, stream, n_paths, path_lo, count, sides)
-    stats = torch.empty(NSLOT * 3, dtype=torch.float64, device=device)
-    paths = torch.empty((4, count), dtype=torch.float64, device=device) if want_paths else None
+def _workspace_bytes(spec: LevelSpec, count: int, device) -> int:
     ws_bytes = int(nat.lib.arv_mlmc_workspace_bytes(count))
     if spec.scheme == "cir_exact":
         # segmented CIR levels (records re-bucketed by lambda between segments,
@@ -270,14 +255,43 @@ def run_level(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, *, path_lo: in
         seg_bytes = int(nat.lib.arv_mlmc_cir_workspace_bytes(count))
         if seg_bytes <= torch.cuda.get_device_properties(device).total_memory // 8:
             ws_bytes = seg_bytes
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
+    return ws_bytes
+
+
+def run_level(spec: LevelSpec, stream: Pcg32Stream, n_paths: int, *, path_lo: int = 0,
+              path_count: Optional[int] = None, want_paths: bool = False, device=None, sides: str = "both",
+              stats_out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+              n_fail_out: Optional[torch.Tensor] = None):
+    """Launch one level; returns (stats device f64[NSLOT,3], paths or None, n_fail or None).
+
+    The stream's counter is not consulted: paths are addressed from output
+    0 of (seed, stream_id) as in the reference's fresh ``level_stream``.
+    ``sides`` ("both", "exact", "approx") skips the other side's work; its
+    payoffs and statistics slots are then unspecified.  ``stats_out``
+    (f64[NSLOT * 3]), ``workspace`` (uint8, at least the level's workspace
+    bytes) and ``n_fail_out`` (int64[1], accumulated into) let a caller that
+    launches many levels on one stream reuse its buffers (stream order keeps
+    the reuse safe).
+    """
+    device = device or dev.require_cuda()
+    count = n_paths - path_lo if path_count is None else path_count
+    if n_paths < 1 or count < 1:
+        raise ConfigError("need at least one path")
+    ns = _native_spec(spec, stream, n_paths, path_lo, count, sides)
+    stats = stats_out if stats_out is not None else torch.empty(NSLOT * 3, dtype=torch.float64, device=device)
+    paths = torch.empty((4, count), dtype=torch.float64, device=device) if want_paths else None
+    ws_bytes = _workspace_bytes(spec, count, device)
+    if workspace is not None and workspace.numel() >= ws_bytes:
+        ws = workspace
+    else:
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
     s = dev.stream_handle(device)
     pp = paths.data_ptr() if paths is not None else None
     n_fail = None
     if spec.scheme == "cir_exact":
         tab = _ncchi2_table(spec)
         st = dev.table_on_device(tab.eval_stacks, torch.float64, device)
-        n_fail = torch.zeros(1, dtype=torch.int64, device=device)
+        n_fail = n_fail_out if n_fail_out is not None else torch.zeros(1, dtype=torch.int64, device=device)
         nat.call("arv_mlmc_cir_exact_level", nat.C.byref(ns), st.data_ptr(), st.shape[1], st.shape[2] - 1,
                  st.shape[3], float(tab.nu), stats.data_ptr(), pp, n_fail.data_ptr(), ws.data_ptr(), ws_bytes, s)
     else:
@@ -494,6 +508,16 @@ def _suite_from(spec: LevelSpec, stats, seconds: float) -> dict:
     }
 
 
+_EVENT_POOL: list = []
+
+
+def _events(n: int) -> list:
+    """n timing events from a pool (creating CUDA events costs host time)."""
+    while len(_EVENT_POOL) < n:
+        _EVENT_POOL.append(torch.cuda.Event(enable_timing=True))
+    return _EVENT_POOL[:n]
+
+
 def estimate_level_suites(specs: list, streams: list, n_pilot: int, group=None) -> list:
     """``estimate_level_suite`` for every level of a pilot in one pass.
 
@@ -520,17 +544,18 @@ def estimate_level_suites(specs: list, streams: list, n_pilot: int, group=None) 
     per, extra = divmod(n_pilot, world)
     lo = rank * per + min(rank, extra)
     cnt = per + (1 if rank < extra else 0)
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(specs) + 1)]
+    # one stats block, one workspace and one failure counter for all levels
+    # (stream-ordered reuse), timing events from a pool
+    allst = torch.empty((len(specs) * NSLOT, 3), dtype=torch.float64, device=device)
+    ws = torch.empty(max(_workspace_bytes(sp, cnt, device) for sp in specs), dtype=torch.uint8, device=device)
+    has_cir = any(sp.scheme == "cir_exact" for sp in specs)
+    n_fail = torch.zeros(1, dtype=torch.int64, device=device) if has_cir else None
+    evs = _events(len(specs) + 1)
     evs[0].record()
-    stats, fails = [], []
     for k, (spec, stream) in enumerate(zip(specs, streams)):
-        st, _, nf = run_level(spec, stream, n_pilot, path_lo=lo, path_count=cnt, device=device)
-        stats.append(st)
-        if nf is not None:
-            fails.append(nf)
+        run_level(spec, stream, n_pilot, path_lo=lo, path_count=cnt, device=device,
+                  stats_out=allst[k * NSLOT:(k + 1) * NSLOT].view(-1), workspace=ws, n_fail_out=n_fail)
         evs[k + 1].record()
-    allst = torch.cat(stats, dim=0)  # (levels * NSLOT, 3)
-    n_fail = torch.stack(fails).sum().reshape(1) if fails else None
     if world > 1:
         import torch.distributed as dist
 
