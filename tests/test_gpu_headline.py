@@ -162,3 +162,28 @@ def test_pdl_table_written_by_previous_kernel(arv, orc, tables_npz):
         call("arv_pcg32_subdyadic_f32", 42, 0, 0, c.data_ptr(), 1, 16, 3, out.data_ptr(), n, s)
         ref = orc.pcg32_subdyadic_f32(42, 0, 0, (base * np.float32(scale)).astype(np.float32), 3, n)
         assert np.array_equal(bits(out), bits(ref)), scale
+
+
+def test_config3_max_size_2_32_samples(arv, orc):
+    """BASELINE config 3's largest single-GPU call: 2^32 samples (16 GiB) in one
+    launch -- 64-bit group indices, > 2^31 outputs, the grid-stride tail --
+    checked against the oracle at the start, across the 2^31 boundary and at
+    the very end (sample i of the call = PCG32 output i)."""
+    n = 1 << 32
+    free, _ = torch.cuda.mem_get_info()
+    if free < 4 * n + (2 << 30):
+        pytest.skip("needs ~18 GiB of free device memory")
+    tab = arv.load_table("subdyadic_linear_k16_s8")
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    arv.Pcg32Stream(42, 0).sample(tab, n, out=out)
+    m = 1 << 18
+    for lo in (0, (1 << 31) - m // 2, n - m):
+        want = orc.pcg32_subdyadic_f32(42, 0, lo, tab.coeffs32, tab.sub_bits, m)
+        assert np.array_equal(bits(out[lo:lo + m]), want.view(np.uint32)), lo
+    del out
+    # a ragged size past 2^32 / 8 groups: the scalar tail of the last group
+    n2 = (1 << 31) + 5
+    out = torch.empty(n2, dtype=torch.float32, device="cuda")
+    arv.Pcg32Stream(42, 0, counter=3).sample(tab, n2, out=out)
+    want = orc.pcg32_subdyadic_f32(42, 0, 3 + n2 - m, tab.coeffs32, tab.sub_bits, m)
+    assert np.array_equal(bits(out[n2 - m:]), want.view(np.uint32))

@@ -535,3 +535,25 @@ def test_gaussian_level_kernels_v2_v3_identical(arv, scheme, tab, level, n0):
         _native.call("arv_set_tuning", 4, 0)
     assert np.array_equal(bits(out[2][1]), bits(out[3][1]))
     assert np.array_equal(bits(out[2][0]), bits(out[3][0]))
+
+
+@pytest.mark.parametrize("scheme", ["euler_maruyama", "milstein"])
+def test_gbm_paths_beyond_2_32(arv, orc, tables_npz, scheme):
+    """Path ids and per-step strides past 2^32 (n_paths_total = 2^33, a shard
+    starting at 2^32 + 7): 64-bit tile starts, lane maps and step jumps
+    against the oracle's own jump-ahead, path by path."""
+    from paper_2012_09715_b200.mlmc import run_level
+
+    lin = arv.load_table("dyadic_linear_k15")
+    level, n_total, lo, cnt = 3, 1 << 33, (1 << 32) + 7, 3001
+    spec = arv.LevelSpec(level=level, scheme=scheme, process=arv.GbmParams(**GBM), rv_source=lin,
+                         kind="four_way", n0=1)
+    _, paths, _ = run_level(spec, arv.level_stream(42, level), n_total, path_lo=lo, path_count=cnt,
+                            want_paths=True)
+    ref = np.stack(orc.gbm_paths(mu=0.05, sigma=0.2, x0=1.0, t_end=1.0, level=level, n0=1,
+                                 milstein=scheme == "milstein", payoff_call=False, strike=1.0,
+                                 coeffs=tables_npz["dyadic_linear_k15"], seed=42, seq=level << 32,
+                                 n_paths=n_total, path_lo=lo, path_hi=lo + cnt))
+    got = paths.cpu().numpy()
+    assert np.array_equal(bits(got[2:]), bits(ref[2:]))
+    np.testing.assert_allclose(got[:2], ref[:2], rtol=1e-13, atol=1e-15)
