@@ -139,3 +139,22 @@ def test_host_pipeline_orders_with_the_callers_stream(K, orc, tabs):
         out = np.empty(u.size)
         K.dyadic_eval(c, u, out)
     assert same(out, orc.dyadic_eval((src * 2.0).cpu().numpy(), u))
+
+
+def test_host_pipeline_concurrent_callers(K, orc, tabs):
+    """Python threads calling the plugin at once (ctypes releases the GIL): the
+    per-device pipeline serialises them and every caller gets its own result."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    c = tabs["dyadic_linear_k15"]
+    us = [u64((1 << 21) + 17 * j, 100 + j) for j in range(6)]
+
+    def work(u):
+        out = np.empty_like(u)
+        K.dyadic_eval(c, u, out)
+        return out
+
+    with ThreadPoolExecutor(6) as ex:
+        outs = list(ex.map(work, us))
+    for u, out in zip(us, outs):
+        assert same(out, orc.dyadic_eval(c, u))
