@@ -187,3 +187,30 @@ def test_config3_max_size_2_32_samples(arv, orc):
     arv.Pcg32Stream(42, 0, counter=3).sample(tab, n2, out=out)
     want = orc.pcg32_subdyadic_f32(42, 0, 3 + n2 - m, tab.coeffs32, tab.sub_bits, m)
     assert np.array_equal(bits(out[n2 - m:]), want.view(np.uint32))
+
+
+def test_sample_host_end_to_end_path(arv, orc):
+    """Pcg32Stream.sample_host (the bench's e2e path): chunked generation with
+    the D2H drained on a side stream into a pinned tensor or a numpy array --
+    identical to the device samples, any chunking, the stream counter advanced;
+    a buffer it could not fill in place is refused."""
+    tab = arv.load_table("subdyadic_linear_k16_s8")
+    n = (1 << 22) + 13
+    dev_out = arv.Pcg32Stream(42, 5, counter=11).sample(tab, n)
+    pinned = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    s = arv.Pcg32Stream(42, 5, counter=11)
+    r = s.sample_host(tab, n, out=pinned, chunk=(1 << 20) + 4)
+    assert r is pinned and s.counter == 11 + n
+    assert np.array_equal(bits(pinned), bits(dev_out))
+    host = np.empty(n, np.float32)
+    arv.Pcg32Stream(42, 5, counter=11).sample_host(tab, n, out=host, chunk=1 << 21, sync=False)
+    torch.cuda.synchronize()
+    assert np.array_equal(host.view(np.uint32), bits(dev_out))
+    auto = arv.Pcg32Stream(42, 5, counter=11).sample_host(tab, n)
+    assert auto.is_pinned() and np.array_equal(bits(auto), bits(dev_out))
+    with pytest.raises(arv.ConfigError):
+        arv.Pcg32Stream(42, 5).sample_host(tab, 1000, out=np.empty(2000, np.float32)[::2])
+    with pytest.raises(arv.ConfigError):
+        arv.Pcg32Stream(42, 5).sample_host(tab, 1000, out=np.empty(999, np.float32))
+    want = orc.pcg32_subdyadic_f32(42, 5, 11 + n - 4096, tab.coeffs32, tab.sub_bits, 4096)
+    assert np.array_equal(host[-4096:].view(np.uint32), want.view(np.uint32))
