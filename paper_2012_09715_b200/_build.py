@@ -71,11 +71,13 @@ def built_hash(path: str) -> str | None:
 
 
 def needs_build() -> bool:
-    """Missing, older than a source, or built from other sources (hash)."""
+    """Missing, or built from other sources.  Content-based (the embedded
+    source hash), not mtime-based: a snapshot copied to another machine may
+    not keep file times, and a library whose sources are unchanged must not
+    be rebuilt there."""
     if not os.path.exists(LIB_PATH):
         return True
-    t = os.path.getmtime(LIB_PATH)
-    return any(os.path.getmtime(p) > t for p in _deps()) or built_hash(LIB_PATH) != source_hash()
+    return built_hash(LIB_PATH) != source_hash()
 
 
 def build(verbose_ptxas: bool = False, force: bool = False, defines=(), out: str | None = None) -> str:
