@@ -260,6 +260,11 @@ ARV_API int arv_ncchi2_inv_cdf_tol(const double *u, const double *lam, int64_t n
 /* Device non-central chi^2 CDF (Poisson-mixture of regularized gammas). */
 ARV_API int arv_ncchi2_cdf(const double *x, const double *lam, int64_t nlam, double nu, double *out, int64_t n,
                    void *stream);
+/* Test hook: out[i] = the exact-side standard normal the Gaussian MLMC level
+ * kernels compute for the 32-bit word words[i] (u = (w + 1/2) 2^-32): AS241
+ * (exact_dist.py:65-126) with fused multiply-adds, a reciprocal-based
+ * division and the kernels' own tail logarithm / square root. */
+ARV_API int arv_test_level_normals(const uint32_t *words, double *out, int64_t n, void *stream);
 
 #ifdef __cplusplus
 }

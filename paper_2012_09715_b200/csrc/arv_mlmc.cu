@@ -25,6 +25,7 @@
 #include "arv_common.cuh"
 #include "arv_eval_dev.cuh"
 #include "arv_ncchi2.cuh"
+#include "arv_logtab.cuh"
 
 namespace arv {
 
@@ -532,8 +533,13 @@ __device__ __forceinline__ double horner(int which, double x) {
     return acc;
 }
 
-// n / d for the positive, well-scaled AS241 denominators: reciprocal estimate,
-// two Newton steps and a residual correction (no special-case path).
+// n / d for the positive, well-scaled AS241 denominators: reciprocal estimate
+// y0 (MUFU.RCP64H: the operand's top 20 mantissa bits, relative error e ~ 2^-20)
+// and one second-order step y = y0 (1 + e + e^2) = (1 - e^3) / d -- three DFMA,
+// ~2^-60 before rounding; the quotient n y is within ~1.5 ulp of n / d.
+#ifndef ARV_GBM_RCP_ORDER2
+#define ARV_GBM_RCP_ORDER2 1  // 0: two Newton steps (four DFMA)
+#endif
 template <bool FMA>
 __device__ __forceinline__ double divide(double n, double d) {
     if constexpr (!FMA) {
@@ -541,13 +547,18 @@ __device__ __forceinline__ double divide(double n, double d) {
     } else {
         double y;
         asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+#if ARV_GBM_RCP_ORDER2
+        const double e = fma(-d, y, 1.0);
+        y = fma(y, fma(e, e, e), y);
+#else
         y = fma(fma(-d, y, 1.0), y, y);
         y = fma(fma(-d, y, 1.0), y, y);
+#endif
 #if ARV_GBM_DIV_CORRECT
         const double q0 = __dmul_rn(n, y);
         return fma(fma(-d, q0, n), y, q0);
 #else
-        return __dmul_rn(n, y);  // within ~1 ulp of n / d (the residual correction costs two DFMA)
+        return __dmul_rn(n, y);
 #endif
     }
 }
@@ -558,11 +569,55 @@ __device__ __forceinline__ double central(double q) {
     return divide<FMA>(__dmul_rn(q, horner<FMA>(kA, r)), horner<FMA>(kB, r));
 }
 
+// -log(v) for a tail element, v = min(u, 1 - u) in [2^-33, 0.075): with
+// v = m 2^e, m in [1, 2), bucket j = top 7 mantissa bits of m and the table
+// (inv_j, T_j = log(inv_j)) of arv_logtab.cuh, m inv_j = 1 + r exactly in the
+// FMA (|r| <= 2^-8) and -log(v) = (-e) ln2 + T_j - log1p(r); log1p by its
+// series through r^6 (truncation < 2^-58).  ~1.1 ulp (tools/make_log_table.py,
+// tests/test_gpu_mlmc.py::test_level_normals_accuracy); 9 FP64 operations where
+// CUDA's log() takes ~25 plus ~20 constant moves.
+__device__ __forceinline__ double neg_log(double v) {
+    const int hi = __double2hiint(v);
+    const int ne = 1023 - (hi >> 20);
+    const double2 tj = __ldg(kLogTab + ((hi >> 13) & 127));
+    const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, __double2loint(v));
+    const double r = fma(m, tj.x, -1.0);
+    double q = fma(r, -1.0 / 6.0, 0.2);
+    q = fma(q, r, -0.25);
+    q = fma(q, r, 1.0 / 3.0);
+    q = fma(q, r, -0.5);
+    const double lp = fma(__dmul_rn(r, r), q, r);
+    return __dsub_rn(fma(static_cast<double>(ne), 0.6931471805599453094, tj.y), lp);
+}
+
+// sqrt(x) for x in [2.5, 24]: MUFU.RSQ64H estimate (~2^-20), one coupled
+// Goldschmidt step (g ~ sqrt x, h ~ 1 / (2 sqrt x) to ~2^-39) and the final
+// residual correction: faithful (< 1 ulp; 0.99 * 2^-53 relative in the CPU
+// emulation), no special-case path (__dsqrt_rn carries one behind a CALL).
+__device__ __forceinline__ double sqrt_mid(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double g = __dmul_rn(x, y), h = __dmul_rn(0.5, y);
+    const double r = fma(-g, h, 0.5);
+    g = fma(g, r, g);
+    h = fma(h, r, h);
+    return fma(fma(-g, g, x), h, g);
+}
+
+#ifndef ARV_GBM_TAIL_CUSTOM
+#define ARV_GBM_TAIL_CUSTOM 1  // 0: CUDA log() and __dsqrt_rn
+#endif
 // |AS241(u)| of a tail element from w = min(u, 1 - u) (exact_dist.py:100-126)
-template <bool FMA>
+// FAR = false: callers whose uniforms carry 32 bits (v >= 2^-33, r <= 4.79)
+// never reach the far-tail E / F rational.
+template <bool FMA, bool FAR = true>
 __device__ __forceinline__ double tail_abs(double w) {
+#if ARV_GBM_TAIL_CUSTOM
+    const double r = FMA ? sqrt_mid(neg_log(w)) : __dsqrt_rn(-log(w));
+#else
     const double r = __dsqrt_rn(-log(w));
-    if (r <= 5.0) {
+#endif
+    if (!FAR || r <= 5.0) {
         const double x = __dsub_rn(r, 1.6);
         return divide<FMA>(horner<FMA>(kC, x), horner<FMA>(kD, x));
     }
@@ -630,7 +685,7 @@ __device__ __forceinline__ void as241_words(const uint32_t (&w)[N], const double
                 buf[pos[k]] = v[k];
             }
         __syncwarp();
-        for (int g = threadIdx.x & 31; g < total; g += 32) buf[g] = tail_abs<FMA>(buf[g]);
+        for (int g = threadIdx.x & 31; g < total; g += 32) buf[g] = tail_abs<FMA, false>(buf[g]);  // PCG32 words only (v >= 2^-33)
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < N; ++k)
@@ -1025,7 +1080,7 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
                 for (int q = t; q < nt; q += NB) {
                     const int slot = list[q];
                     const double pv = zbuf[slot];
-                    zbuf[slot] = copysign(g2::tail_abs<FMA>(fabs(pv)), pv);  // upper tail positive (exact_dist.py:124-126)
+                    zbuf[slot] = copysign(g2::tail_abs<FMA, false>(fabs(pv)), pv);  // upper tail positive (exact_dist.py:124-126)
                 }
             }
             __syncthreads();
@@ -1058,6 +1113,25 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
             }
         }
         cta_moments<ARV_NKIND>(d, valid, parts + tile * 3 * ARV_NKIND);
+    }
+}
+
+// Test hook: the level kernels' exact-side normal of each 32-bit word
+// (u = (w + 1/2) 2^-32): the FMA central rational, or the tail evaluation
+// (neg_log, sqrt_mid, C / D rational) -- the arithmetic k_gaussian_level_v2 /
+// _v3 run, element by element.
+__global__ void __launch_bounds__(256) k_level_normals(const uint32_t *__restrict__ w, double *__restrict__ out,
+                                                       int64_t n) {
+    constexpr bool FMA = ARV_GBM_FMA_EXACT != 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t wi[1] = {w[i]};
+        double z[1];
+        if (g2::central_words<1, FMA>(wi, z)) {
+            const double t = g2::tail_abs<FMA, false>(g2::reflected(wi[0]));
+            z[0] = wi[0] >> 31 ? t : -t;
+        }
+        out[i] = z[0];
     }
 }
 
@@ -1720,6 +1794,13 @@ int arv_ncchi2_cdf(const double *x, const double *lam, int64_t nlam, double nu, 
     k_ncchi2_cdf<<<stream_grid(n, 256, 8), 256, 0, as_stream(stream)>>>(x, lam, nlam, nu, out, n);
     note_launch();
     return check_launch("arv_ncchi2_cdf");
+}
+
+int arv_test_level_normals(const uint32_t *words, double *out, int64_t n, void *stream) {
+    if (n <= 0) return n < 0 ? set_error(ARV_ERR_CONFIG, "negative n") : ARV_OK;
+    k_level_normals<<<stream_grid(n, 256, 8), 256, 0, as_stream(stream)>>>(words, out, n);
+    note_launch();
+    return check_launch("arv_test_level_normals");
 }
 
 #if ARV_NC_COUNT

@@ -557,3 +557,35 @@ def test_gbm_paths_beyond_2_32(arv, orc, tables_npz, scheme):
     got = paths.cpu().numpy()
     assert np.array_equal(bits(got[2:]), bits(ref[2:]))
     np.testing.assert_allclose(got[:2], ref[:2], rtol=1e-13, atol=1e-15)
+
+
+def test_level_normals_accuracy(arv):
+    """The level kernels' exact-side normal (FMA central rational; tails with
+    the kernels' own -log / sqrt and the C/D rational) against the oracle's
+    AS241 f64 (exact_dist.py:65-126, separately rounded, libm log): the MLMC
+    contract is statistical, this pins the evaluation itself to <= 1e-15
+    relative over random words, both central thresholds and both stream ends."""
+    from oracle import oracle as orc
+    from paper_2012_09715_b200 import _native
+
+    rng = np.random.default_rng(7)
+    edges = np.array([0, 1, 2, 3, 0x13333332, 0x13333333, 0x13333334, 0x7FFFFFFF, 0x80000000, 0xECCCCCCB,
+                      0xECCCCCCC, 0xECCCCCCD, 0xFFFFFFFD, 0xFFFFFFFE, 0xFFFFFFFF], dtype=np.uint32)
+    # random words, the two tails densely, and every octave of the lower tail
+    lo_tail = rng.integers(0, 0x13333333, 1 << 18, dtype=np.uint64).astype(np.uint32)
+    hi_tail = (0xFFFFFFFF - rng.integers(0, 0x13333333, 1 << 18, dtype=np.uint64)).astype(np.uint32)
+    octaves = np.concatenate([(np.uint64(1) << np.uint64(b)) + rng.integers(0, 1 << b, 4096, dtype=np.uint64)
+                              for b in range(0, 29)]).astype(np.uint32)
+    w = np.concatenate([edges, rng.integers(0, 1 << 32, 1 << 20, dtype=np.uint64).astype(np.uint32), lo_tail,
+                        hi_tail, octaves])
+    wd = torch.from_numpy(w.view(np.int32)).cuda()
+    out = torch.empty(w.size, dtype=torch.float64, device="cuda")
+    _native.call("arv_test_level_normals", wd.data_ptr(), out.data_ptr(), w.size,
+                 torch.cuda.current_stream().cuda_stream)
+    got = out.cpu().numpy()
+    u = (w.astype(np.float64) + 0.5) * 2.0 ** -32
+    ref = orc.as241_f64(u)
+    rel = np.abs(got - ref) / np.abs(ref)
+    assert np.all(np.isfinite(got))
+    assert rel.max() <= 1e-15, (rel.max(), hex(int(w[rel.argmax()])))
+    assert np.array_equal(np.signbit(got), u < 0.5)
