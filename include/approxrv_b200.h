@@ -131,8 +131,10 @@ ARV_API int arv_pcg32_subdyadic_f32(uint64_t seed, uint64_t stream_id, uint64_t 
  * for a word w with w >> 9 == k.  mode 0 = the general evaluator
  * (k_pcg32_subdyadic); mode 1 = the degree-1 signed-table evaluator
  * (k_pcg32_linsigned, sub_bits <= 4) including its per-table exactness check
- * and fallback; *fast (device int32[1], may be NULL) receives 1 if the
- * signed evaluator ran, 0 if the table failed the check. */
+ * and fallback; mode 2 = the lane-private-table evaluator (k_pcg32_linlane,
+ * sub_bits <= 4; scalar and packed-pair forms); *fast (device int32[1], may
+ * be NULL) receives 1 if the signed / lane evaluator ran, 0 if the table
+ * failed the check. */
 ARV_API int arv_lattice_subdyadic_f32(const float *coeffs, int degree, int K, int sub_bits, int mode, float *out,
                                       int *fast, void *stream);
 /* exact comparators: AS241 of the same f32-lattice uniforms, f64 / f32 out */
@@ -174,6 +176,10 @@ ARV_API int arv_store_probe_ex(float *out, int64_t n, int mode, void *stream);
  * 0 (default), 2 (per-iteration warp tail lists) or 3 (phased tail list);
  * both give bit-identical paths and statistics. */
 #define ARV_TUNE_GBM_KERNEL 4
+/* ARV_TUNE_LANE_MIN_N = log2 of the smallest degree-1 sub-interval call that
+ * takes the lane-private-table kernel (k_pcg32_linlane: conflict-free shared
+ * memory lookups, 57 KB staged per CTA); default 24; < 0: never. */
+#define ARV_TUNE_LANE_MIN_N 5
 ARV_API int arv_set_tuning(int key, int value);
 
 /* ---- nested MLMC level kernels ------------------------------------------

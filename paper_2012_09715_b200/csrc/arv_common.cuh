@@ -105,6 +105,33 @@ __device__ __forceinline__ uint64_t pack2f(float lo, float hi) {
 }
 __device__ __forceinline__ uint32_t lo32(uint64_t x) { return static_cast<uint32_t>(x); }
 __device__ __forceinline__ uint32_t hi32(uint64_t x) { return static_cast<uint32_t>(x >> 32); }
+
+// One PCG32 LCG step s' = M s + inc.  The low product and the increment go
+// through one IMAD.WIDE; the two cross products are then accumulated on top
+// of its high word in place (2 IMAD): 3 instructions and a 2-IMAD dependency
+// chain per step, where `M * s + inc` compiles to 3 IMAD + 1 add.  `mlo` is
+// the multiplier's low word in a register (with the literal the compiler
+// turns the widening multiply into a 64-bit one and ptxas adds a stray
+// zero high word per step).
+#ifndef ARV_LCG3
+#define ARV_LCG3 1
+#endif
+__device__ __forceinline__ void lcg_step_pcg(uint32_t &lo, uint32_t &hi, uint64_t inc, uint32_t mlo) {
+#if ARV_LCG3
+    constexpr uint32_t mhi = static_cast<uint32_t>(kPcgMult >> 32);
+    const uint64_t r = static_cast<uint64_t>(lo) * mlo + inc;
+    uint32_t rl, h;  // inline PTX: written as C, the compiler re-associates the sum into 2 IMAD + IADD3
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(rl), "=r"(h) : "l"(r));
+    asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(h) : "r"(hi), "r"(mlo));
+    asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(h) : "r"(lo), "r"(mhi));
+    lo = rl;
+    hi = h;
+#else
+    const uint64_t s = lcg_step(pack2(lo, hi), kPcgMult, inc);
+    lo = lo32(s);
+    hi = hi32(s);
+#endif
+}
 __device__ __forceinline__ uint64_t f32x2_add(uint64_t a, uint64_t b) {
     uint64_t r;
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -160,9 +187,7 @@ __device__ __forceinline__ uint32_t pcg32_output(uint64_t old) {
 // hi * 2^k) on the FMA pipe, balancing the ALU-heavy XSH-RR.  m19 = 2^19,
 // m5 = 2^5 must arrive in registers (not immediates), or ptxas folds the
 // multiply back into a shift.
-__device__ __forceinline__ uint32_t pcg32_output_fma(uint64_t old, uint32_t m19, uint32_t m5) {
-    const uint32_t lo = static_cast<uint32_t>(old);
-    const uint32_t hi = static_cast<uint32_t>(old >> 32);
+__device__ __forceinline__ uint32_t pcg32_output_fma(uint32_t lo, uint32_t hi, uint32_t m19, uint32_t m5) {
 #if ARV_PCG_IMADHI >= 1
     const uint32_t rot = __umulhi(hi, m5);  // hi >> 27
 #else

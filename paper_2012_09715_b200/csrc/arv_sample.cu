@@ -44,6 +44,7 @@ constexpr int kSignedUnroll = ARV_SIGNED_UNROLL;  // the signed-table generator 
 // Process-wide launch shape knobs (arv_set_tuning); defaults from sweeps.
 static int g_group = 8;        // samples per thread-group: 4 (v4) or 8 (v8)
 static int g_ctas_per_sm = 0;  // CTAs per SM (256 threads each); 0 = auto (see gen_grid)
+static int64_t g_lane_min_n = int64_t{1} << 24;  // calls of at least this many samples take the lane-table kernel (< 0: never)
 extern int g_cir_segment;      // arv_mlmc.cu
 extern int g_gbm_kernel;       // arv_mlmc.cu
 
@@ -65,22 +66,27 @@ struct GenArgs {
 // once and shares the state; each thread then walks only its 8 low bits
 // (powers of one affine map commute).  A full 24-bit walk per thread was ~20%
 // of a thread's work at 2^24 samples.
-__device__ __forceinline__ uint64_t group_start(const GenArgs &a, uint64_t g0) {
-    __shared__ uint64_t s_cta;
+template <int LB>  // log2(blockDim.x); s_cta: a shared-memory slot for the CTA's state
+__device__ __forceinline__ uint64_t group_start(const GenArgs &a, uint64_t g0, uint64_t &s_cta) {
     if (threadIdx.x == 0) {
         uint64_t s = a.s_base;
-        const uint64_t hb = g0 >> 8;
+        const uint64_t hb = g0 >> LB;
 #pragma unroll 1
-        for (int i = 8; i < kJumpBits && (hb >> (i - 8)) != 0; ++i)
+        for (int i = LB; i < kJumpBits && (hb >> (i - LB)) != 0; ++i)
             if ((g0 >> i) & 1u) s = a.pow2[i].a * s + a.pow2[i].c;
         s_cta = s;
     }
     __syncthreads();
     uint64_t s = s_cta;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < LB; ++i)
         if ((g0 >> i) & 1u) s = a.pow2[i].a * s + a.pow2[i].c;
     return s;
+}
+template <int LB = 8>
+__device__ __forceinline__ uint64_t group_start(const GenArgs &a, uint64_t g0) {
+    __shared__ uint64_t s_cta;
+    return group_start<LB>(a, g0, s_cta);
 }
 
 static GenArgs make_gen_args(uint64_t seed, uint64_t stream_id, uint64_t offset, int64_t n,
@@ -150,6 +156,7 @@ __device__ __forceinline__ void gen_run(const GenArgs &a, uint32_t *__restrict__
     const uint64_t z = static_cast<uint64_t>(threadIdx.x) * a.zero;  // 0, but not provably uniform
     const uint64_t inc = a.inc + z;
     const Affine st{a.stride.a + z, a.stride.c + z};
+    const uint32_t mlo = static_cast<uint32_t>(kPcgMult) + static_cast<uint32_t>(z);
     const uint32_t m19 = (1u << 19) + static_cast<uint32_t>(z), m5 = 32u + static_cast<uint32_t>(z);
     // Trip count once; the loop runs on a 32-bit counter and a pointer bump.
     // host-computed quotient / remainder: no 64-bit division per thread
@@ -159,11 +166,14 @@ __device__ __forceinline__ void gen_run(const GenArgs &a, uint32_t *__restrict__
 #pragma unroll U
     for (uint32_t it = 0; it < iters; ++it) {
         uint32_t w[G];
+        uint32_t slo, shi;  // the state as two words: the low product is then one widening multiply
+        asm("mov.b64 {%0, %1}, %2;" : "=r"(slo), "=r"(shi) : "l"(s));
 #pragma unroll
         for (int i = 0; i < G; ++i) {
-            w[i] = pcg32_output_fma(s, m19, m5);
-            s = i < G - 1 ? lcg_step(s, kPcgMult, inc) : lcg_step(s, st.a, st.c);
+            w[i] = pcg32_output_fma(slo, shi, m19, m5);
+            if (i < G - 1) lcg_step_pcg(slo, shi, inc, mlo);
         }
+        s = lcg_step(pack2(slo, shi), st.a, st.c);
         uint32_t r[G];
 #pragma unroll
         for (int i = 0; i < G; i += 2) eval_two(eval, w[i], w[i + 1], r[i], r[i + 1]);
@@ -198,7 +208,7 @@ template <int G, class Eval, class Stage>
 __device__ __forceinline__ void gen_loop_vec(const GenArgs &a, uint32_t *__restrict__ out, const Eval &eval,
                                              const Stage &stage) {
     const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t s = group_start(a, g0);
+    const uint64_t s = group_start<>(a, g0);
     pdl_wait();
     stage();
     gen_run<G>(a, out, eval, s, g0);
@@ -415,53 +425,147 @@ __device__ __forceinline__ float lin_at(float c0, float c1, int64_t m) {
     return __fadd_rn(__fmul_rn(c1, v), c0);
 }
 
+// Entry e = (E - kSignedE0) << b | sub of the signed tables: its coefficients
+// (c0, c1) from the natural-layout coeffs (2, K, 2^b), and whether the signed
+// evaluation is bit-exact on it (c1 times the power of two `c1_scale` is
+// exact, and no lattice point |vh| = m + 1/2 of the entry gives z == 0).
+__device__ __forceinline__ bool linsigned_entry(const float *__restrict__ coeffs, int K, int b, int e, float c1_scale,
+                                                float &c0, float &c1s) {
+    const int nsub = 1 << b;
+    const int E = kSignedE0 + (e >> b), sub = e & (nsub - 1);
+    const int j = 149 - E;  // octave 1..23
+    const int jj = j < K ? j : K;
+    const int ss = j < K ? sub : 0;
+    c0 = __ldg(coeffs + static_cast<int64_t>(jj - 1) * nsub + ss);
+    const float c1 = __ldg(coeffs + (static_cast<int64_t>(K) + jj - 1) * nsub + ss);
+    c1s = __fmul_rn(c1, c1_scale);
+    bool ok = isfinite(c0) && isfinite(c1) && __fmul_rn(c1s, 1.0f / c1_scale) == c1;
+    // lattice points |vh| = m + 1/2 inside [lo, hi) of this entry
+    const float lo = __uint_as_float(static_cast<uint32_t>(E) << 23 | static_cast<uint32_t>(sub) << (23 - b));
+    const float hi = __uint_as_float((static_cast<uint32_t>(E) << 23) + (static_cast<uint32_t>(sub + 1) << (23 - b)));
+    const int64_t m_lo = static_cast<int64_t>(ceilf(lo - 0.5f));
+    const int64_t m_hi = static_cast<int64_t>(ceilf(hi - 0.5f)) - 1;
+    if (m_lo <= m_hi) {
+        // z is monotone in m over the entry (v exact and increasing, RN
+        // monotone), so its exact zeros form one contiguous run.  Ends of
+        // one sign: no zero.  A sign change (the fit crosses 0 near
+        // v = 1/2): bisect with strict signs at both ends -- a run of
+        // zeros between them is always hit by some midpoint.
+        const float za = lin_at(c0, c1, m_lo), zb = lin_at(c0, c1, m_hi);
+        if (za == 0.0f || zb == 0.0f || !(isfinite(za) && isfinite(zb))) {
+            ok = false;
+        } else if ((za > 0.0f) != (zb > 0.0f)) {
+            int64_t lo_m = m_lo, hi_m = m_hi;
+            while (hi_m - lo_m > 1) {
+                const int64_t mid = lo_m + (hi_m - lo_m) / 2;
+                const float zm = lin_at(c0, c1, mid);
+                if (zm == 0.0f) {
+                    ok = false;
+                    break;
+                }
+                if ((zm > 0.0f) == (za > 0.0f)) lo_m = mid;
+                else hi_m = mid;
+            }
+        }
+    }
+    return ok;
+}
+
 // Stage natural-layout coeffs (2, K, 2^b) into the signed table; returns the
 // CTA-wide verdict that the signed evaluation is bit-exact for this table.
 __device__ __forceinline__ bool stage_linsigned(float2 *sm, const float *__restrict__ coeffs, int K, int b) {
-    const int nsub = 1 << b;
     const int neg = 1 << (8 + b);
     bool ok = true;
     for (int e = threadIdx.x; e < (23 << b); e += blockDim.x) {
-        const int E = kSignedE0 + (e >> b), sub = e & (nsub - 1);
-        const int j = 149 - E;  // octave 1..23
-        const int jj = j < K ? j : K;
-        const int ss = j < K ? sub : 0;
-        const float c0 = __ldg(coeffs + static_cast<int64_t>(jj - 1) * nsub + ss);
-        const float c1 = __ldg(coeffs + (static_cast<int64_t>(K) + jj - 1) * nsub + ss);
-        const float c1s = __fmul_rn(c1, 0x1p-23f);
-        ok &= isfinite(c0) && isfinite(c1) && __fmul_rn(c1s, 0x1p23f) == c1;
-        // lattice points |vh| = m + 1/2 inside [lo, hi) of this entry
-        const float lo = __uint_as_float(static_cast<uint32_t>(E) << 23 | static_cast<uint32_t>(sub) << (23 - b));
-        const float hi = __uint_as_float((static_cast<uint32_t>(E) << 23) + (static_cast<uint32_t>(sub + 1) << (23 - b)));
-        const int64_t m_lo = static_cast<int64_t>(ceilf(lo - 0.5f));
-        const int64_t m_hi = static_cast<int64_t>(ceilf(hi - 0.5f)) - 1;
-        if (m_lo <= m_hi) {
-            // z is monotone in m over the entry (v exact and increasing, RN
-            // monotone), so its exact zeros form one contiguous run.  Ends of
-            // one sign: no zero.  A sign change (the fit crosses 0 near
-            // v = 1/2): bisect with strict signs at both ends -- a run of
-            // zeros between them is always hit by some midpoint.
-            const float za = lin_at(c0, c1, m_lo), zb = lin_at(c0, c1, m_hi);
-            if (za == 0.0f || zb == 0.0f || !(isfinite(za) && isfinite(zb))) {
-                ok = false;
-            } else if ((za > 0.0f) != (zb > 0.0f)) {
-                int64_t lo_m = m_lo, hi_m = m_hi;
-                while (hi_m - lo_m > 1) {
-                    const int64_t mid = lo_m + (hi_m - lo_m) / 2;
-                    const float zm = lin_at(c0, c1, mid);
-                    if (zm == 0.0f) {
-                        ok = false;
-                        break;
-                    }
-                    if ((zm > 0.0f) == (za > 0.0f)) lo_m = mid;
-                    else hi_m = mid;
-                }
-            }
-        }
+        float c0, c1s;
+        ok &= linsigned_entry(coeffs, K, b, e, 0x1p-23f, c0, c1s);
         sm[e] = make_float2(c0, c1s);
         sm[neg + e] = make_float2(-c0, c1s);
     }
     return __syncthreads_and(ok) != 0;
+}
+
+// The signed table with lane-private copies ("lane table"): the headline
+// kernel's shared-memory lookups without bank conflicts.  On the signed table
+// above a warp's 32 random LDS.64 take 5.1 wavefronts of the SM's shared-memory
+// data path (ncu: l1tex data-pipe 93% busy -- the kernel's actual limiter,
+// not HBM and not instruction issue); here they take the minimum of 2.
+//   vh = (i + 1/2) 2^-13 (same construction with the magic scaled by 2^-13),
+//   so |vh| in [2^-14, 2^9) is a normal f16 and  h = cvt.rz.f16(vh)  is
+//   s | E5 | m10 with E5 = 1..23 (octave 24 - E5) and the top mantissa bits
+//   the sub-interval (truncation: the index never rounds up).
+// Row r = h >> (10 - b) starts at byte (h & mask), mask = 0xFFFF << (10 - b):
+// for b <= 3 a row is >= 128 bytes and holds 16 copies of the entry
+// (c0 or -c0, c1 2^-10), one per lane of a half-warp at byte 8 (lane & 15), so
+// the 16 lanes one LDS.64 wavefront serves always hit 16 different bank pairs.
+// The address is one LOP3, (h & mask) | lane_off, and rows 0 .. 2^b - 1 (E5 = 0)
+// are never addressed, so `lane_off` carries the table base less those rows.
+// Same exactness conditions as the signed table (c1 2^-10 exact, no z == 0).
+constexpr int kLaneBlockLog2 = 9;                              // 512 threads per CTA
+constexpr int kLaneBlock = 1 << kLaneBlockLog2;
+constexpr int kLaneTableBytes = 55 << 10;                      // rows 2^b .. (56 << b) - 1: 56320 for every b
+constexpr int kLaneScratch = kLaneTableBytes + 16;             // after the CTA state slot: the parked entries
+constexpr int kLaneBytes = kLaneScratch + 8 * (23 << 4);       // dynamic shared memory per CTA (b <= 4)
+constexpr int kLaneMaxBits = 4;                                // b = 4: 8 copies (2-way conflicts at worst)
+
+template <bool OR>  // the table's row 0 is at shared address 0: (h & mask) | lane_base is the address
+struct EvalLinLane {
+    uint32_t lane_base;  // shared byte address of row 0 plus this lane's copy offset
+    uint32_t mask;       // 0xFFFF << (10 - b) & 0xFFFF
+    __device__ __forceinline__ uint32_t addr(uint32_t h) const {
+        return OR ? ((h & mask) | lane_base) : ((h & mask) + lane_base);
+    }
+    __device__ __forceinline__ static uint32_t magic(uint32_t w) {
+        return 0x44C00000u + static_cast<uint32_t>(static_cast<int32_t>(w) >> 9);  // (12582912 + i) 2^-13
+    }
+    __device__ __forceinline__ uint32_t operator()(uint32_t w) const {
+        const float vh = __fadd_rn(__fadd_rn(__uint_as_float(magic(w)), -1536.0f), 0x1p-14f);
+        uint32_t h;
+        asm("{.reg .b16 t; cvt.rz.f16.f32 t, %1; mov.b32 %0, {t, 0};}" : "=r"(h) : "f"(vh));
+        const float2 c = lds_f32x2(addr(h));
+        return __float_as_uint(__fadd_rn(__fmul_rn(c.y, vh), c.x));
+    }
+    static constexpr bool kHasPair = true;
+    __device__ __forceinline__ void pair(uint32_t w0, uint32_t w1, uint32_t &r0, uint32_t &r1) const {
+        const uint64_t g = pack2(magic(w0), magic(w1));
+        const uint64_t vh = f32x2_add(f32x2_add(g, kMinusMagic2), kHalf2);
+        const float v0 = __uint_as_float(lo32(vh)), v1 = __uint_as_float(hi32(vh));
+        uint32_t h;  // {f16(v1), f16(v0)}, truncated
+        asm("cvt.rz.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(v1), "f"(v0));
+        const float2 c0 = lds_f32x2(addr(h));
+        const float2 c1 = lds_f32x2(addr(h >> 16));
+        r0 = __float_as_uint(__fadd_rn(__fmul_rn(c0.y, v0), c0.x));
+        r1 = __float_as_uint(__fadd_rn(__fmul_rn(c1.y, v1), c1.x));
+    }
+    static constexpr uint64_t kMinusMagic2 = 0xC4C00000C4C00000ull;  // {-1536, -1536}
+    static constexpr uint64_t kHalf2 = 0x3880000038800000ull;        // {2^-14, 2^-14}
+};
+
+// Stage the lane table (`sm` points at row 2^b: the E5 = 0 rows are not
+// allocated); verdict as stage_linsigned.  Two phases so that the stores are
+// conflict-free: the (23 << b) entries are checked and parked in `scratch`
+// (one per thread), then every thread writes copy (i % copies) of entry
+// (i / copies) -- consecutive lanes fill consecutive 8-byte slots of a row.
+__device__ __forceinline__ bool stage_linlane(char *sm, float2 *scratch, const float *__restrict__ coeffs, int K, int b) {
+    const int row_bytes = 1 << (10 - b);
+    const int copies = row_bytes >= 128 ? 16 : row_bytes / 8;
+    const int n_entries = 23 << b;
+    bool ok = true;
+    for (int e = threadIdx.x; e < n_entries; e += blockDim.x) {
+        float c0, c1s;
+        ok &= linsigned_entry(coeffs, K, b, e, 0x1p-10f, c0, c1s);
+        scratch[e] = make_float2(c0, c1s);
+    }
+    ok = __syncthreads_and(ok) != 0;
+    for (int i = threadIdx.x; i < n_entries * copies; i += blockDim.x) {
+        const int e = i / copies, c = i - e * copies;
+        const float2 v = scratch[e];
+        // e = (E5 - 1) << b | sub; row (E5 << b | sub) = e + 2^b, stored less the 2^b skipped rows
+        reinterpret_cast<float2 *>(sm + static_cast<size_t>(e) * row_bytes)[c] = v;
+        reinterpret_cast<float2 *>(sm + (static_cast<size_t>(e) + (32 << b)) * row_bytes)[c] = make_float2(-v.x, v.y);
+    }
+    __syncthreads();
+    return ok;
 }
 
 // --------------------------------------------------------------- kernels --
@@ -515,7 +619,7 @@ __global__ void __launch_bounds__(256, ARV_GEN_MINB) k_pcg32_linsigned(GenArgs a
 #endif
     extern __shared__ float4 smem4[];
     const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t s = group_start(a, g0);
+    const uint64_t s = group_start<>(a, g0);
     pdl_wait();
     float2 *tab = reinterpret_cast<float2 *>(smem4);
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
@@ -524,6 +628,44 @@ __global__ void __launch_bounds__(256, ARV_GEN_MINB) k_pcg32_linsigned(GenArgs a
         // sustained 210.3 vs 211.3 / 216.4 us (tools/gen_tune.py)
         gen_run<MODE, kSignedUnroll>(a, out, EvalLinSigned{sbase - 8u * (kSignedE0 << b), 23 - b,
                                                            8u + threadIdx.x * a.zero32}, s, g0);
+    } else {  // CTA-uniform
+        float *sm = reinterpret_cast<float *>(smem4);
+        __syncthreads();
+        stage_subdyadic<1>(sm, coeffs, K, b);
+        gen_run<MODE>(a, out, EvalSubDyadic<1>{sbase - 4u * (kLatticeE0 << b), 23 - b, 4u + threadIdx.x * a.zero32}, s,
+                      g0);
+    }
+}
+
+// The headline kernel for large calls: lane-private table copies, 512 threads
+// per CTA (3 CTAs per SM share 168 KB of tables).  Tables failing the
+// exactness checks fall back to EvalSubDyadic<1> like k_pcg32_linsigned.
+template <int MODE>
+__global__ void __launch_bounds__(kLaneBlock, 3) k_pcg32_linlane(GenArgs a, const float *__restrict__ coeffs, int K, int b,
+                                                                 uint32_t *out) {
+    static_assert(MODE == 4 || MODE == 8, "vector stores only");
+#if ARV_GEN_PDL
+    asm volatile("griddepcontrol.launch_dependents;");
+#endif
+    // No static shared memory in this kernel: the table is the first thing in
+    // the CTA's window, behind the 1 KB the driver reserves -- exactly the
+    // 2^b unaddressed rows (1 KB for every b), so row 0 sits at shared address
+    // 0 and the lookup address needs no base add.  Checked at run time; any
+    // other placement takes the variant with the add.
+    extern __shared__ float4 smem4[];
+    char *tab = reinterpret_cast<char *>(smem4);
+    const uint64_t g0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t s = group_start<kLaneBlockLog2>(a, g0, *reinterpret_cast<uint64_t *>(tab + kLaneTableBytes));
+    pdl_wait();
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
+    if (stage_linlane(tab, reinterpret_cast<float2 *>(tab + kLaneScratch), coeffs, K, b)) {
+        const uint32_t row_bytes = 1u << (10 - b);
+        const uint32_t copies = row_bytes >= 128 ? 16 : row_bytes / 8;
+        const uint32_t lane_base = sbase - 1024u + 8u * (threadIdx.x & (copies - 1));  // 2^b rows = 1 KB
+        uint32_t mask = (0xFFFFu << (10 - b)) & 0xFFFFu;
+        asm volatile("mov.b32 %0, %0;" : "+r"(mask));  // opaque: one LOP3 (h & mask) | lane_base per lookup
+        if (sbase == 1024u) gen_run<MODE, kSignedUnroll>(a, out, EvalLinLane<true>{lane_base, mask}, s, g0);
+        else gen_run<MODE, kSignedUnroll>(a, out, EvalLinLane<false>{lane_base, mask}, s, g0);
     } else {  // CTA-uniform
         float *sm = reinterpret_cast<float *>(smem4);
         __syncthreads();
@@ -548,6 +690,28 @@ __global__ void __launch_bounds__(256) k_lattice_sub(const float *__restrict__ c
     if constexpr (MODE == 1) {
         use_signed = stage_linsigned(reinterpret_cast<float2 *>(smem4), coeffs, K, b);
         if (fast && blockIdx.x == 0 && threadIdx.x == 0) *fast = use_signed ? 1 : 0;
+    }
+    if constexpr (MODE == 2) {
+        char *tab = reinterpret_cast<char *>(smem4);
+        const bool lane_ok = stage_linlane(tab, reinterpret_cast<float2 *>(tab + kLaneScratch), coeffs, K, b);
+        if (fast && blockIdx.x == 0 && threadIdx.x == 0) *fast = lane_ok ? 1 : 0;
+        if (lane_ok) {
+            const uint32_t row_bytes = 1u << (10 - b);
+            const uint32_t copies = row_bytes >= 128 ? 16 : row_bytes / 8;
+            const EvalLinLane<false> ev{sbase - 1024u + 8u * (threadIdx.x & (copies - 1)), (0xFFFFu << (10 - b)) & 0xFFFFu};
+            // pairs through pair() (the generator's path), the odd point out through operator()
+            for (int k = 2 * k0; k < kLatticeN; k += 2 * stride) {
+                const uint32_t w0 = (static_cast<uint32_t>(k) << 9) | ((k * 0x9E3779B1u) >> 23);
+                const uint32_t w1 = (static_cast<uint32_t>(k + 1) << 9) | (((k + 1) * 0x9E3779B1u) >> 23);
+                if ((k >> 1) & 1) {
+                    ev.pair(w0, w1, out[k], out[k + 1]);
+                } else {
+                    out[k] = ev(w0);
+                    out[k + 1] = ev(w1);
+                }
+            }
+            return;
+        }
     }
     if (use_signed) {
         const EvalLinSigned ev{sbase - 8u * (kSignedE0 << b), 23 - b, 8u};
@@ -627,15 +791,16 @@ constexpr int64_t kMinPerThread = 64;
 // samples) run 5/3 waves instead: the generators then finish 1.2-1.7% sooner
 // (2^28: sub-interval 0.1935 -> 0.1911 ms, constant 0.1663 -> 0.1635 ms;
 // 2^26 and below keep one wave, where the extra CTAs cost 2-20%).
-static int gen_grid(const void *fn, int64_t n, int mode, size_t smem = 0) {
+static int gen_grid(const void *fn, int64_t n, int mode, size_t smem = 0, int block = kGenBlock,
+                    bool extra_wave = true) {
     int per_sm = g_ctas_per_sm;
     if (per_sm <= 0) {
-        const int64_t want = n / (static_cast<int64_t>(device_sm_count()) * kGenBlock * kMinPerThread);
-        const int occ = resident_ctas(fn, kGenBlock, smem);
+        const int64_t want = n / (static_cast<int64_t>(device_sm_count()) * block * kMinPerThread);
+        const int occ = resident_ctas(fn, block, smem);
         per_sm = static_cast<int>(want < 1 ? 1 : (want < occ ? want : occ));
-        if (want >= 16 * occ) per_sm = occ + (2 * occ) / 3;
+        if (extra_wave && want >= 16 * occ) per_sm = occ + (2 * occ) / 3;
     }
-    return stream_grid((n + mode - 1) / mode, kGenBlock, per_sm);
+    return stream_grid((n + mode - 1) / mode, block, per_sm);
 }
 
 template <class Eval>
@@ -669,6 +834,33 @@ template <int D>
 static void launch_subdyadic(uint64_t seed, uint64_t sid, uint64_t offset, const float *coeffs, int K, int sub_bits,
                              float *out, int64_t n, int mode, void *stream) {
     const bool signed_tab = ARV_GEN_SIGNED && D == 1 && mode != 1 && sub_bits <= kSignedMaxBits;
+    // Large calls: the lane-private table (57 KB staged per 512-thread CTA pays
+    // off from a few million samples on; g_lane_min_n, ARV_TUNE_LANE_MIN_N).
+    if (signed_tab && sub_bits <= kLaneMaxBits && g_lane_min_n >= 0 && n >= g_lane_min_n) {
+        const void *lfn = mode == 8 ? (const void *)k_pcg32_linlane<8> : (const void *)k_pcg32_linlane<4>;
+        static bool attr_set[2] = {false, false};
+        if (!attr_set[mode == 8]) {
+            cudaFuncSetAttribute(lfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kLaneBytes);
+            attr_set[mode == 8] = true;
+        }
+        // one wave of 3 CTAs per SM: 174.3 us vs 175.5 us for 5/3 waves at 2^28 (tools/gen_tune_lane.py)
+        const int grid = gen_grid(lfn, n, mode, kLaneBytes, kLaneBlock, false);
+        const GenArgs a = make_gen_args(seed, sid, offset, n, static_cast<int64_t>(grid) * kLaneBlock, mode);
+        uint32_t *o = reinterpret_cast<uint32_t *>(out);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kLaneBlock);
+        cfg.dynamicSmemBytes = kLaneBytes;
+        cfg.stream = as_stream(stream);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = ARV_GEN_PDL;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (mode == 8) cudaLaunchKernelEx(&cfg, k_pcg32_linlane<8>, a, coeffs, K, sub_bits, o);
+        else cudaLaunchKernelEx(&cfg, k_pcg32_linlane<4>, a, coeffs, K, sub_bits, o);
+        return;
+    }
     const void *fn = signed_tab  ? (mode == 8 ? (const void *)k_pcg32_linsigned<8> : (const void *)k_pcg32_linsigned<4>)
                      : mode == 8 ? (const void *)k_pcg32_subdyadic<D, 8>
                      : mode == 4 ? (const void *)k_pcg32_subdyadic<D, 4>
@@ -729,6 +921,10 @@ int arv_set_tuning(int key, int value) {
         case ARV_TUNE_GBM_KERNEL:
             if (value != 0 && value != 2 && value != 3) return set_error(ARV_ERR_CONFIG, "gbm kernel must be 0, 2 or 3");
             g_gbm_kernel = value;
+            return ARV_OK;
+        case ARV_TUNE_LANE_MIN_N:  // log2 of the smallest call that takes the lane-table kernel; < 0: never
+            if (value > 40) return set_error(ARV_ERR_CONFIG, "lane_min_n (log2) must be <= 40");
+            g_lane_min_n = value < 0 ? -1 : (int64_t{1} << value);
             return ARV_OK;
         case ARV_TUNE_CTAS_PER_SM:
             if (value < 0 || value > 32) return set_error(ARV_ERR_CONFIG, "ctas_per_sm must be in [0 (auto), 32]");
@@ -801,16 +997,19 @@ int arv_lattice_subdyadic_f32(const float *coeffs, int degree, int K, int sub_bi
                               void *stream) {
     if (degree != 1) return set_error(ARV_ERR_CONFIG, "lattice hook: degree must be 1");
     if (K < 1 || K > 40) return set_error(ARV_ERR_CONFIG, "octave count K must be in [1, 40], got %d", K);
-    if (sub_bits < 0 || sub_bits > (mode == 1 ? kSignedMaxBits : 5))
+    if (sub_bits < 0 || sub_bits > (mode == 1 ? kSignedMaxBits : mode == 2 ? kLaneMaxBits : 5))
         return set_error(ARV_ERR_CONFIG, "sub_bits out of range for mode %d", mode);
-    const size_t smem = std::max<size_t>(sizeof(float2) * linsigned_entries(sub_bits), sizeof(float) * 2 * kLatticePlane);
+    const size_t smem = std::max<size_t>({sizeof(float2) * linsigned_entries(sub_bits), sizeof(float) * 2 * kLatticePlane,
+                                          mode == 2 ? size_t{kLaneBytes} : size_t{0}});
     cudaStream_t s = as_stream(stream);
     uint32_t *o = reinterpret_cast<uint32_t *>(out);
     if (smem > 48 * 1024) {
         cudaFuncSetAttribute((const void *)k_lattice_sub<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute((const void *)k_lattice_sub<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute((const void *)k_lattice_sub<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
-    if (mode == 1) k_lattice_sub<1><<<4 * device_sm_count(), 256, smem, s>>>(coeffs, K, sub_bits, o, fast);
+    if (mode == 2) k_lattice_sub<2><<<2 * device_sm_count(), 256, smem, s>>>(coeffs, K, sub_bits, o, fast);
+    else if (mode == 1) k_lattice_sub<1><<<4 * device_sm_count(), 256, smem, s>>>(coeffs, K, sub_bits, o, fast);
     else k_lattice_sub<0><<<4 * device_sm_count(), 256, smem, s>>>(coeffs, K, sub_bits, o, fast);
     note_launch();
     return check_launch("arv_lattice_subdyadic_f32");

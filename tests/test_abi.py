@@ -83,6 +83,9 @@ class TestValidationBeforeCuda:
             nat.call("arv_ncchi2_inv_cdf", None, None, 1, -1.0, None, None, None, 4, None)
         with pytest.raises(errors.ConfigError, match="group must be"):
             nat.call("arv_set_tuning", 1, 5)
+        with pytest.raises(errors.ConfigError, match="lane_min_n"):
+            nat.call("arv_set_tuning", 5, 41)
+        nat.call("arv_set_tuning", 5, 24)
         assert nat.launch_count() == 0
 
     def test_zero_length_is_a_noop(self, nat):

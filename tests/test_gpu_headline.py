@@ -69,11 +69,11 @@ def test_shipped_tables_whole_lattice(arv, orc, tables_npz, lattice_u, name, b):
     else:
         c = tables_npz[name].astype(np.float32)
     want = orc.subdyadic_eval32(c, b, lattice_u)
-    for mode in (0, 1):
+    for mode in (0, 1, 2):
         got, fast = lattice_eval(c, b, mode)
         assert np.array_equal(bits(got), bits(want)), (name, mode)
-        if mode == 1:
-            assert fast == 1, "shipped table must take the signed-table fast path"
+        if mode:
+            assert fast == 1, "shipped table must take the signed-table / lane-table fast path"
 
 
 @pytest.mark.parametrize("b", [0, 1, 2, 3, 4])
@@ -81,9 +81,11 @@ def test_shipped_tables_whole_lattice(arv, orc, tables_npz, lattice_u, name, b):
 def test_random_tables_whole_lattice(arv, orc, lattice_u, b, K):
     rng = np.random.default_rng(100 * K + b)
     c = random_table(rng, K, b)
-    got, fast = lattice_eval(c, b, 1)
-    assert fast == 1
-    assert np.array_equal(bits(got), bits(orc.subdyadic_eval32(c, b, lattice_u)))
+    want = orc.subdyadic_eval32(c, b, lattice_u)
+    for mode in (1, 2):  # signed table, lane-private table (scalar and packed-pair forms)
+        got, fast = lattice_eval(c, b, mode)
+        assert fast == 1
+        assert np.array_equal(bits(got), bits(want)), mode
 
 
 def test_fallback_on_exact_zero(arv, orc, lattice_u):
@@ -99,23 +101,46 @@ def test_fallback_on_exact_zero(arv, orc, lattice_u):
     want = orc.subdyadic_eval32(c, 3, lattice_u)
     zero = (want == 0) & (lattice_u < 0.5)
     assert zero.any() and np.signbit(orc.subdyadic_eval32(c, 3, (np.float32(1) - lattice_u[zero]))).all()
-    got, fast = lattice_eval(c, 3, 1)
-    assert fast == 0
-    assert np.array_equal(bits(got), bits(want))
-    # the fused generator takes the same fallback: upper-half samples of that
-    # point come out as -0.0 like the reference
+    for mode in (1, 2):
+        got, fast = lattice_eval(c, 3, mode)
+        assert fast == 0
+        assert np.array_equal(bits(got), bits(want))
+    # the fused generators take the same fallback: upper-half samples of that
+    # point come out as -0.0 like the reference (signed-table kernel, then the
+    # lane-table kernel that large calls take)
     n = 1 << 22
+    want = bits(orc.pcg32_subdyadic_f32(11, 2, 0, c, 3, n))
     out = arv.Pcg32Stream(11, 2).sample(_subtable(arv, c, 3), n)
-    assert np.array_equal(bits(out), bits(orc.pcg32_subdyadic_f32(11, 2, 0, c, 3, n)))
+    assert np.array_equal(bits(out), want)
+    with lane_min_n(20):
+        out = arv.Pcg32Stream(11, 2).sample(_subtable(arv, c, 3), n)
+    assert np.array_equal(bits(out), want)
 
 
 def test_fallback_on_inexact_slope_scaling(arv, orc, lattice_u):
     rng = np.random.default_rng(8)
     c = random_table(rng, 12, 2)
     c[1, 4, 1] = np.float32(3e-36)  # c1 * 2^-23 is subnormal and would round
-    got, fast = lattice_eval(c, 2, 1)
-    assert fast == 0
-    assert np.array_equal(bits(got), bits(orc.subdyadic_eval32(c, 2, lattice_u)))
+    for mode in (1, 2):  # (3e-36 2^-10 is subnormal too)
+        got, fast = lattice_eval(c, 2, mode)
+        assert fast == 0
+        assert np.array_equal(bits(got), bits(orc.subdyadic_eval32(c, 2, lattice_u)))
+
+
+import contextlib
+
+
+@contextlib.contextmanager
+def lane_min_n(log2n):
+    """ARV_TUNE_LANE_MIN_N (key 5): calls of >= 2^log2n samples take the
+    lane-table kernel (default 24); < 0 never."""
+    from paper_2012_09715_b200._native import call
+
+    call("arv_set_tuning", 5, log2n)
+    try:
+        yield
+    finally:
+        call("arv_set_tuning", 5, 24)
 
 
 def _subtable(arv, c, b):
@@ -130,8 +155,40 @@ def test_fused_generator_every_sub_bits(arv, orc, b):
     rng = np.random.default_rng(b)
     c = random_table(rng, 18, b)
     n = (1 << 20) + 5
+    want = bits(orc.pcg32_subdyadic_f32(42, 0, 3, c, b, n))
     out = arv.Pcg32Stream(42, 0, counter=3).sample(_subtable(arv, c, b), n)
-    assert np.array_equal(bits(out), bits(orc.pcg32_subdyadic_f32(42, 0, 3, c, b, n)))
+    assert np.array_equal(bits(out), want)
+    with lane_min_n(0):  # every call through the lane-table kernel (b <= 4; b = 5 stays general)
+        out = arv.Pcg32Stream(42, 0, counter=3).sample(_subtable(arv, c, b), n)
+    assert np.array_equal(bits(out), want)
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 4097, (1 << 24) + 3])
+def test_lane_kernel_ragged_sizes_and_alignment(arv, orc, n):
+    """The lane-table kernel (512-thread CTAs, its own start-state walk) on
+    ragged sizes, v8 / v4 store alignment and a non-zero stream offset."""
+    tab = arv.load_table("subdyadic_linear_k16_s8")
+    buf = torch.empty(n + 8, dtype=torch.float32, device="cuda")
+    for shift in (0, 4):  # 32-byte (v8) and 16-byte (v4) aligned outputs
+        out = buf[shift:shift + n]
+        with lane_min_n(0):
+            arv.Pcg32Stream(9, 4, counter=12345).sample(tab, n, out=out)
+        m = min(n, 1 << 16)
+        for lo in (0, n - m):
+            want = orc.pcg32_subdyadic_f32(9, 4, 12345 + lo, tab.coeffs32, tab.sub_bits, m)
+            assert np.array_equal(bits(out[lo:lo + m]), want.view(np.uint32)), (n, shift, lo)
+
+
+def test_lane_kernel_threshold_is_bit_identical(arv):
+    """Below / above ARV_TUNE_LANE_MIN_N the same call takes the signed-table
+    or the lane-table kernel: identical output."""
+    tab = arv.load_table("subdyadic_linear_k16_s8")
+    n = (1 << 25) + 40
+    with lane_min_n(-1):
+        a = arv.Pcg32Stream(42, 0).sample(tab, n)
+    with lane_min_n(0):
+        b = arv.Pcg32Stream(42, 0).sample(tab, n)
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))
 
 
 def test_config2_full_output_sha256(arv, hashes):
@@ -158,10 +215,14 @@ def test_pdl_table_written_by_previous_kernel(arv, orc, tables_npz):
         # a long-running kernel, then the table-writing kernel, then the generator
         big = torch.empty(1 << 26, dtype=torch.float32, device="cuda")
         call("arv_store_probe", big.data_ptr(), big.numel(), s)
-        torch.mul(src, scale, out=c)
-        call("arv_pcg32_subdyadic_f32", 42, 0, 0, c.data_ptr(), 1, 16, 3, out.data_ptr(), n, s)
         ref = orc.pcg32_subdyadic_f32(42, 0, 0, (base * np.float32(scale)).astype(np.float32), 3, n)
-        assert np.array_equal(bits(out), bits(ref)), scale
+        for lm in (24, 0):  # signed-table kernel, lane-table kernel
+            c.zero_()
+            call("arv_store_probe", big.data_ptr(), big.numel(), s)
+            torch.mul(src, scale, out=c)
+            with lane_min_n(lm):
+                call("arv_pcg32_subdyadic_f32", 42, 0, 0, c.data_ptr(), 1, 16, 3, out.data_ptr(), n, s)
+            assert np.array_equal(bits(out), bits(ref)), (scale, lm)
 
 
 def test_config3_max_size_2_32_samples(arv, orc):
