@@ -366,13 +366,52 @@ def config1_entry(arv, _native, device, offset: int, peak: float, steps: int = 2
         b.record()
     torch.cuda.synchronize()
     probe = sum(a.elapsed_time(b) for a, b in evs) * 1e-3 / len(evs)
+    # the same event sandwich around an (almost) empty launch: the fixed cost inside every figure above
+    for a, b in evs:
+        _native.call("arv_store_probe", scratch.data_ptr(), scratch.numel(), s)
+        a.record()
+        _native.call("arv_store_probe", out.data_ptr(), 8, s)
+        b.record()
+    torch.cuda.synchronize()
+    empty = sum(a.elapsed_time(b) for a, b in evs) * 1e-3 / len(evs)
+    # Back to back without the per-launch event pair: a CUDA graph of 16 launches over a ring of
+    # 8 output buffers (512 MiB > L2: no launch writes lines the previous ones left in L2);
+    # programmatic dependent launch overlaps each launch's start-state walk with the previous tail.
+    table = arv.load_table(tname)
+    ring = [torch.empty(n, dtype=torch.float32, device=device) for _ in range(8)]
+    side = torch.cuda.Stream(device=device)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for i in range(8):
+            arv.Pcg32Stream(42, 0, counter=offset).sample(table, n, out=ring[i])
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            for i in range(16):
+                arv.Pcg32Stream(42, 0, counter=offset + i * n).sample(table, n, out=ring[i % 8])
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(10):
+            g.replay()
+        b.record()
+        b.synchronize()
+        ring_t = a.elapsed_time(b) * 1e-3 / 160
+    torch.cuda.current_stream().wait_stream(side)
+    ring_bw = n * BYTES_PER_SAMPLE / ring_t / 1e9
     return {"workload": wl, "value": n / per_launch, "unit": "samples/s", "us_per_launch": per_launch * 1e6,
             "steps": steps, "gpu_launches": int(launches),
             "l2": "output < L2: each launch timed alone, 512 MiB store sweep flushes L2 in between",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "algorithmic_bytes_per_launch": n * BYTES_PER_SAMPLE,
                          "store_probe_same_size_us": probe * 1e6,
-                         "frac_of_store_probe_same_size": probe / per_launch}}
+                         "frac_of_store_probe_same_size": probe / per_launch,
+                         "empty_launch_same_protocol_us": empty * 1e6},
+            "back_to_back": {"us_per_launch": ring_t * 1e6, "value": n / ring_t, "unit": "samples/s",
+                             "achieved": ring_bw, "frac": ring_bw / peak, "gpu_launches": 160,
+                             "l2": "ring of 8 output buffers (512 MiB > L2), 10 replays of a CUDA graph of 16 launches, "
+                                   "one event pair around all of them"}}
 
 
 def e2e_plugin(arv, device, steps: int = 3) -> dict:

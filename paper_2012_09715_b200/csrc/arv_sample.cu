@@ -578,6 +578,11 @@ __global__ void __launch_bounds__(256, ARV_GEN_MINB) k_gen_simple(GenArgs a, uin
 template <int MODE, int KIND>
 __global__ void __launch_bounds__(256, ARV_GEN_MINB) k_pcg32_constant(GenArgs a, const float *__restrict__ values, int q,
                                                         uint32_t *out) {
+#if ARV_GEN_PDL
+    // let the next kernel on the stream start its CTAs (start-state walk) as ours retire;
+    // our own table reads and stores come after griddepcontrol.wait (gen_loop_vec)
+    asm volatile("griddepcontrol.launch_dependents;");
+#endif
     if constexpr (KIND == 0) {
         extern __shared__ float4 smem4[];
         float *sm = reinterpret_cast<float *>(smem4);
@@ -969,7 +974,17 @@ int arv_pcg32_constant_f32(uint64_t seed, uint64_t stream_id, uint64_t offset, c
     const GenArgs a = make_gen_args(seed, stream_id, offset, n, T, mode == 1 ? 4 : mode);
     uint32_t *o = reinterpret_cast<uint32_t *>(out);
     void *args[] = {(void *)&a, (void *)&values, (void *)&q, (void *)&o};
-    cudaLaunchKernel(fn, dim3(grid), dim3(kGenBlock), args, smem, as_stream(stream));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kGenBlock);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (ARV_GEN_PDL && mode != 1) ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelExC(&cfg, fn, args);
     note_launch();
     return check_launch("arv_pcg32_constant_f32");
 }

@@ -275,3 +275,28 @@ def test_sample_host_end_to_end_path(arv, orc):
         arv.Pcg32Stream(42, 5).sample_host(tab, 1000, out=np.empty(999, np.float32))
     want = orc.pcg32_subdyadic_f32(42, 5, 11 + n - 4096, tab.coeffs32, tab.sub_bits, 4096)
     assert np.array_equal(host[-4096:].view(np.uint32), want.view(np.uint32))
+
+
+def test_pdl_constant_table_written_by_previous_kernel(arv, orc, tables_npz):
+    """The config-1 generator is launched with programmatic dependent launch
+    too: its value table is staged after griddepcontrol.wait, so values written
+    by the kernel just before it on the stream are the ones used, and
+    back-to-back launches into one buffer keep their order."""
+    from paper_2012_09715_b200 import _device as dev
+    from paper_2012_09715_b200._native import call
+
+    base = tables_npz["constant_q10_l1"].astype(np.float32)
+    src = torch.from_numpy(base).cuda()
+    v = torch.zeros_like(src)
+    n = (1 << 22) + 24
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    big = torch.empty(1 << 26, dtype=torch.float32, device="cuda")
+    s = dev.stream_handle()
+    for scale in (1.0, -3.0, 0.25):
+        v.zero_()
+        call("arv_store_probe", big.data_ptr(), big.numel(), s)
+        call("arv_pcg32_constant_f32", 1, 1, 0, src.data_ptr(), 10, out.data_ptr(), n, s)  # overwritten below
+        torch.mul(src, scale, out=v)
+        call("arv_pcg32_constant_f32", 42, 0, 7, v.data_ptr(), 10, out.data_ptr(), n, s)
+        ref = orc.pcg32_constant_f32(42, 0, 7, (base * np.float32(scale)).astype(np.float32), n)
+        assert np.array_equal(bits(out), bits(ref)), scale
