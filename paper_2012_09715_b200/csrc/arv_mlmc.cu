@@ -1032,8 +1032,13 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
 #pragma unroll
             for (int k = 0; k < N; ++k) {
                 const double v = g2::reflected(w[k]);
-                // a tail element parks +-v: the sign marks the upper tail
-                zbuf[(k0 + k) * NB + t] = (pb >> k) & 1u ? (w[k] >> 31 ? v : -v) : z[k];
+                // a tail element parks +-v: the sign marks the upper tail (v > 0: the sign
+                // bit is the complement of w's top bit -- one LOP3 and a predicated second
+                // store instead of two 64-bit selects)
+                zbuf[(k0 + k) * NB + t] = z[k];
+                if ((pb >> k) & 1u)
+                    zbuf[(k0 + k) * NB + t] =
+                        __hiloint2double(__double2hiint(v) | static_cast<int>(~w[k] & 0x80000000u), __double2loint(v));
                 a[k] = g2::table<DEG>(smd, w[k], v, cap, K1);
             }
             pend |= pb << k0;
