@@ -697,10 +697,13 @@ __device__ __forceinline__ void as241_words(const uint32_t (&w)[N], const double
     }
 }
 
-// v = min(u, 1 - u) = (w' + 1/2) 2^-32, w' = w (u < 1/2) or ~w (exact)
+// v = min(u, 1 - u) = (w' + 1/2) 2^-32, w' = w (u < 1/2) or ~w -- as
+// 1/2 - |q| with q = u - 1/2 = (1 + u) - 3/2, both subtractions exact (all
+// three are multiples of 2^-33 below 1).  q is the central rational's own
+// argument (the compiler shares it), so v costs one FP64 add with a free |.|
+// instead of a second bit assembly of 1 + u'.
 __device__ __forceinline__ double reflected(uint32_t w) {
-    const uint32_t wr = w ^ static_cast<uint32_t>(static_cast<int32_t>(w) >> 31);
-    return __dsub_rn(one_plus_u32(wr), 1.0);
+    return __dsub_rn(0.5, fabs(__dsub_rn(one_plus_u32(w), 1.5)));
 }
 
 // Approximate side of one element: dyadic_eval (DEG >= 1; table interleaved
@@ -716,8 +719,9 @@ __device__ __forceinline__ double table(const double *sm, uint32_t w, double v, 
         return sm[idx];
     } else {
         constexpr int S = (DEG + 2) & ~1;
-        const uint32_t neg = static_cast<uint32_t>(static_cast<int32_t>(w) >> 31);
-        int idx = __clz(w ^ neg);  // 1022 - expo(v), _kernels.pyx:36
+        // 1022 - expo(v) (_kernels.pyx:36) read off v's exponent field: v in [2^-33, 1/2)
+        // is (w' + 1/2) 2^-32, so it equals clz(w') (a shift and an add-min)
+        int idx = 1022 - (__double2hiint(v) >> 20);
         idx = idx < cap ? idx : cap;
         ARV_DCHECK(idx >= 0 && idx <= cap);
         const double *c = sm + idx * S;
@@ -731,7 +735,7 @@ __device__ __forceinline__ double table(const double *sm, uint32_t w, double v, 
             for (int d = DEG - 1; d >= 0; --d) z = __dadd_rn(__dmul_rn(z, v), c[d]);
         }
         // out = pred ? z : -z (u < 1/2 <=> top bit of w clear)
-        return __hiloint2double(__double2hiint(z) ^ static_cast<int>(neg & 0x80000000u), __double2loint(z));
+        return __hiloint2double(__double2hiint(z) ^ static_cast<int>(w & 0x80000000u), __double2loint(z));
     }
 }
 }  // namespace g2
