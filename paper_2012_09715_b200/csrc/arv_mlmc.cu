@@ -834,9 +834,17 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
             return step(x, dw, dt, mudt);
         }
     };
+    // Exact-side step from the normal z (dW = sqrt(dt_f) z).  GBM Euler-Maruyama with
+    // FMA steps: sg sqrt(dt_f) is folded into one constant, x + x (mu dt + (sg sqrt(dt_f)) z)
+    // -- one FP64 multiply per step fewer (the level kernels are FP64-pipe-bound).
+    const double sgsq = __dmul_rn(sg, sq_f);
+    auto step_z = [&](double x, double z, double dt, double mudt) -> double {
+        if constexpr (GBM && FMA && ARV_GBM_FMA_STEP && !MIL) return fma(x, fma(sgsq, z, mudt), x);
+        else return step_e(x, __dmul_rn(sq_f, z), dt, mudt);
+    };
     auto pair_step = [&](double z0, double z1, double w0, double w1) {
-        xf_e = step_e(step_e(xf_e, __dmul_rn(sq_f, z0), dt_f, mudt_f), __dmul_rn(sq_f, z1), dt_f, mudt_f);
-        xc_e = step_e(xc_e, __dmul_rn(sq_f, __dadd_rn(z0, z1)), dt_c, mudt_c);
+        xf_e = step_z(step_z(xf_e, z0, dt_f, mudt_f), z1, dt_f, mudt_f);
+        xc_e = step_z(xc_e, __dadd_rn(z0, z1), dt_c, mudt_c);
         xf_a = step(step(xf_a, __dmul_rn(sq_f, w0), dt_f, mudt_f), __dmul_rn(sq_f, w1), dt_f, mudt_f);
         xc_a = step(xc_a, __dmul_rn(sq_f, __dadd_rn(w0, w1)), dt_c, mudt_c);
     };
@@ -879,7 +887,7 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
         uint32_t w[1] = {draw()};
         double v[1] = {g2::reflected(w[0])}, z[1] = {0.0};
         if (we) g2::as241_words<1, FMA>(w, v, z, buf);
-        if (we) xf_e = step_e(xf_e, __dmul_rn(sq_f, z[0]), dt_f, mudt_f);
+        if (we) xf_e = step_z(xf_e, z[0], dt_f, mudt_f);
         if (wa) xf_a = step(xf_a, __dmul_rn(sq_f, g2::table<DEG>(smd, w[0], v[0], cap, K1)), dt_f, mudt_f);
     }
     double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
@@ -1019,6 +1027,11 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
                 return step(x, dw, dt, mudt);
             }
         };
+        const double sgsq = __dmul_rn(sg, sq_f);  // as k_gaussian_level_v2
+        auto step_z = [&](double x, double z, double dt, double mudt) -> double {
+            if constexpr (GBM && FMA && ARV_GBM_FMA_STEP && !MIL) return fma(x, fma(sgsq, z, mudt), x);
+            else return step_e(x, __dmul_rn(sq_f, z), dt, mudt);
+        };
         auto draw = [&]() -> uint32_t {
             const uint32_t w = pcg32_output(s);
             s = st.a * s + st.c;
@@ -1097,10 +1110,10 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
             int k = 0;
             for (; k + 2 <= L; k += 2) {
                 const double z0 = zbuf[k * NB + t], z1 = zbuf[(k + 1) * NB + t];
-                xf_e = step_e(step_e(xf_e, __dmul_rn(sq_f, z0), dt_f, mudt_f), __dmul_rn(sq_f, z1), dt_f, mudt_f);
-                xc_e = step_e(xc_e, __dmul_rn(sq_f, __dadd_rn(z0, z1)), dt_c, mudt_c);
+                xf_e = step_z(step_z(xf_e, z0, dt_f, mudt_f), z1, dt_f, mudt_f);
+                xc_e = step_z(xc_e, __dadd_rn(z0, z1), dt_c, mudt_c);
             }
-            if (k < L) xf_e = step_e(xf_e, __dmul_rn(sq_f, zbuf[k * NB + t]), dt_f, mudt_f);
+            if (k < L) xf_e = step_z(xf_e, zbuf[k * NB + t], dt_f, mudt_f);
             ++blk;
         }
         double d[ARV_NKIND] = {0.0, 0.0, 0.0, 0.0, 0.0};
