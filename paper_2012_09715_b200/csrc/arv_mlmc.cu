@@ -175,30 +175,56 @@ __device__ __forceinline__ double cir_step(double x, double dw, double dt, doubl
 }
 
 // ------------------------------------------------------ CTA reduction --
+// Warp sums of 5 values per lane with the xor-butterfly's summation tree
+// (pairs at lane distance 16, then 8, 4, 2, 1 -- the tree the plain
+// `s += shfl_xor(s, o)` loop builds in every lane, so the results are bit for
+// bit those of the per-value butterflies), but the first four values share
+// the lanes: at distance 16 the warp's halves exchange one of each pair of
+// values and keep the other, at distance 8 the quarters do the same, and from
+// there one value per lane is left.  6 + 5 64-bit shuffles and adds instead
+// of 25.  Results: value 0 / 1 / 2 / 3 in lanes [0, 8) / [16, 24) / [8, 16) /
+// [24, 32) of `c`, value 4 in every lane of `e`.
+struct WarpSum5 {
+    double c, e;
+};
+__device__ __forceinline__ WarpSum5 warp_sum5(const double (&x)[5], int lane) {
+    const bool h16 = lane & 16, h8 = lane & 8;
+    const double a = (h16 ? x[1] : x[0]) + __shfl_xor_sync(0xffffffffu, h16 ? x[0] : x[1], 16);
+    const double b = (h16 ? x[3] : x[2]) + __shfl_xor_sync(0xffffffffu, h16 ? x[2] : x[3], 16);
+    double c = (h8 ? b : a) + __shfl_xor_sync(0xffffffffu, h8 ? a : b, 8);
+    double e = x[4];
+    e += __shfl_xor_sync(0xffffffffu, e, 16);
+    e += __shfl_xor_sync(0xffffffffu, e, 8);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+        e += __shfl_xor_sync(0xffffffffu, e, o);
+    }
+    return {c, e};
+}
+// which of the first four values lane group (lane >> 3) holds in WarpSum5::c
+__device__ __forceinline__ int warp_sum5_kind(int lane) { return ((lane >> 4) & 1) | ((lane >> 2) & 2); }
+
 // Two-pass (count, mean, M2) of NK values per thread over the CTA.
 template <int NK, int BS = kLevelBlock>
 __device__ __forceinline__ void cta_moments(const double (&d)[NK], bool valid, double *partial_out) {
-    __shared__ double red[NK][BS / 32];
+    static_assert(NK == 5, "warp_sum5");
+    // One buffer per pass: a call's first-pass sums are last read before its second
+    // barrier and its second-pass sums before the next call's first barrier, so
+    // back-to-back calls (one per tile) need no barrier on entry -- three per call.
+    __shared__ double red[2][NK][BS / 32];
     __shared__ double mean_sh[NK];
-    __shared__ int cnt_sh;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int cnt_w = __popc(__ballot_sync(0xffffffffu, valid));
-    if (threadIdx.x == 0) cnt_sh = 0;
-    __syncthreads();
-    if (lane == 0) atomicAdd(&cnt_sh, cnt_w);
     double s[NK];
 #pragma unroll
-    for (int k = 0; k < NK; ++k) {
-        s[k] = valid ? d[k] : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
-        if (lane == 0) red[k][warp] = s[k];
-    }
-    __syncthreads();
-    const int count = cnt_sh;
+    for (int k = 0; k < NK; ++k) s[k] = valid ? d[k] : 0.0;
+    WarpSum5 w = warp_sum5(s, lane);
+    if ((lane & 7) == 0) red[0][warp_sum5_kind(lane)][warp] = w.c;
+    if (lane == 0) red[0][4][warp] = w.e;
+    const int count = __syncthreads_count(valid);
     if (threadIdx.x < NK) {
         double t = 0.0;
-        for (int w = 0; w < BS / 32; ++w) t += red[threadIdx.x][w];
+        for (int i = 0; i < BS / 32; ++i) t += red[0][threadIdx.x][i];
         mean_sh[threadIdx.x] = count > 0 ? t / count : 0.0;
     }
     __syncthreads();
@@ -206,17 +232,14 @@ __device__ __forceinline__ void cta_moments(const double (&d)[NK], bool valid, d
     for (int k = 0; k < NK; ++k) {
         const double dv = valid ? d[k] - mean_sh[k] : 0.0;
         s[k] = dv * dv;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
     }
-    __syncthreads();  // everyone has read mean_sh / red
-#pragma unroll
-    for (int k = 0; k < NK; ++k)
-        if (lane == 0) red[k][warp] = s[k];
+    w = warp_sum5(s, lane);
+    if ((lane & 7) == 0) red[1][warp_sum5_kind(lane)][warp] = w.c;
+    if (lane == 0) red[1][4][warp] = w.e;
     __syncthreads();
     if (threadIdx.x < NK) {
         double t = 0.0;
-        for (int w = 0; w < BS / 32; ++w) t += red[threadIdx.x][w];
+        for (int i = 0; i < BS / 32; ++i) t += red[1][threadIdx.x][i];
         double *o = partial_out + 3 * threadIdx.x;
         o[0] = count;
         o[1] = mean_sh[threadIdx.x];
@@ -791,9 +814,13 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
         }
     }
     const int64_t ntiles = (A.path_count + kLevelBlock - 1) / kLevelBlock;
-    // start state of this CTA's current tile
-    uint64_t tile_s = path_start_state(A, static_cast<uint64_t>(A.path_lo) + static_cast<uint64_t>(blockIdx.x) * kLevelBlock);
+    // start state of this CTA's current tile: one thread (of another warp than the
+    // stride map's) walks the bits of the path index, the rest read it after the barrier
+    __shared__ uint64_t tile_s0;
+    if (threadIdx.x == 32)
+        tile_s0 = path_start_state(A, static_cast<uint64_t>(A.path_lo) + static_cast<uint64_t>(blockIdx.x) * kLevelBlock);
     __syncthreads();
+    uint64_t tile_s = tile_s0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i = tile * kLevelBlock + threadIdx.x;
     const bool valid = i < A.path_count;
@@ -992,8 +1019,12 @@ __global__ void __launch_bounds__(kLevelBlock, ARV_GBM_V2_MINB) k_gaussian_level
         }
     }
     const int64_t ntiles = (A.path_count + NB - 1) / NB;
-    uint64_t tile_s = path_start_state(A, static_cast<uint64_t>(A.path_lo) + static_cast<uint64_t>(blockIdx.x) * NB);
+    // start state of the CTA's first tile: one thread (of another warp than the
+    // stride map's) walks the bits of the path index, the rest read it after the barrier
+    __shared__ uint64_t tile_s0;
+    if (t == 32) tile_s0 = path_start_state(A, static_cast<uint64_t>(A.path_lo) + static_cast<uint64_t>(blockIdx.x) * NB);
     __syncthreads();
+    uint64_t tile_s = tile_s0;
     unsigned blk = 0;  // running block index: selects the tail counter
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t i = tile * NB + t;
