@@ -843,11 +843,8 @@ static void launch_subdyadic(uint64_t seed, uint64_t sid, uint64_t offset, const
     // off from a few million samples on; g_lane_min_n, ARV_TUNE_LANE_MIN_N).
     if (signed_tab && sub_bits <= kLaneMaxBits && g_lane_min_n >= 0 && n >= g_lane_min_n) {
         const void *lfn = mode == 8 ? (const void *)k_pcg32_linlane<8> : (const void *)k_pcg32_linlane<4>;
-        static bool attr_set[2] = {false, false};
-        if (!attr_set[mode == 8]) {
-            cudaFuncSetAttribute(lfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kLaneBytes);
-            attr_set[mode == 8] = true;
-        }
+        // per call: the attribute is per device, and a call of >= 2^24 samples does not notice it
+        cudaFuncSetAttribute(lfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kLaneBytes);
         // one wave of 3 CTAs per SM: 174.3 us vs 175.5 us for 5/3 waves at 2^28 (tools/gen_tune_lane.py)
         const int grid = gen_grid(lfn, n, mode, kLaneBytes, kLaneBlock, false);
         const GenArgs a = make_gen_args(seed, sid, offset, n, static_cast<int64_t>(grid) * kLaneBlock, mode);

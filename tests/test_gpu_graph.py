@@ -52,6 +52,34 @@ def test_generator_calls_replay_from_a_graph(orc):
     assert torch.equal(first, out)
 
 
+def test_lane_table_kernel_replays_from_a_graph(orc):
+    """A call large enough for the lane-table headline kernel (>= 2^24 samples,
+    59 KB of opted-in dynamic shared memory) captures and replays as well."""
+    import paper_2012_09715_b200 as arv
+
+    sub = arv.load_table("subdyadic_linear_k16_s8")
+    n = (1 << 24) + 16
+    out = torch.empty((2, n), dtype=torch.float32, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        arv.Pcg32Stream(42, 0).sample(sub, n, out=out[0])
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    s = arv.Pcg32Stream(42, 3)
+    with torch.cuda.graph(g):
+        for i in range(2):
+            s.sample(sub, n, out=out[i])
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    m = 1 << 16
+    for i in range(2):
+        for lo in (0, n - m):
+            want = orc.pcg32_subdyadic_f32(42, 3, i * n + lo, sub.coeffs32, sub.sub_bits, m)
+            assert np.array_equal(bits(out[i, lo:lo + m]), want.view(np.uint32)), (i, lo)
+
+
 def test_dropin_eval_replays_from_a_graph(orc, tables_npz):
     from paper_2012_09715_b200 import _kernels
 
