@@ -513,6 +513,8 @@ struct EvalLinLane {
     uint32_t lane_base;  // shared byte address of row 0 plus this lane's copy offset
     uint32_t mask;       // 0xFFFF << (10 - b) & 0xFFFF
     __device__ __forceinline__ uint32_t addr(uint32_t h) const {
+        // rows E5 = 1 .. 23 of either sign: byte offsets [1 KB, 24 KB) and [33 KB, 56 KB) from row 0
+        ARV_DCHECK(((h & mask) & 0x7FFFu) >= 1024u && ((h & mask) & 0x7FFFu) < 24576u);
         return OR ? ((h & mask) | lane_base) : ((h & mask) + lane_base);
     }
     __device__ __forceinline__ static uint32_t magic(uint32_t w) {
@@ -559,6 +561,7 @@ __device__ __forceinline__ bool stage_linlane(char *sm, float2 *scratch, const f
     ok = __syncthreads_and(ok) != 0;
     for (int i = threadIdx.x; i < n_entries * copies; i += blockDim.x) {
         const int e = i / copies, c = i - e * copies;
+        ARV_DCHECK(e < n_entries && (static_cast<size_t>(e) + (32 << b) + 1) * row_bytes <= kLaneTableBytes);
         const float2 v = scratch[e];
         // e = (E5 - 1) << b | sub; row (E5 << b | sub) = e + 2^b, stored less the 2^b skipped rows
         reinterpret_cast<float2 *>(sm + static_cast<size_t>(e) * row_bytes)[c] = v;

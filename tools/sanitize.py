@@ -3,7 +3,7 @@
 
     compute-sanitizer --tool racecheck python tools/sanitize.py
 
-Covers the fused generators (v8 / v4 / scalar store paths, signed-table and
+Covers the fused generators (v8 / v4 / scalar store paths, signed-table, lane-table and
 general evaluators, PDL launch), the lattice hook, the Gaussian level kernels
 (v2 with the warp-wide AS241 tail list; the Philox kernel), the atomic-ticket
 chunk finalize (more than 2048 CTA partials), the CIR exact level in its
@@ -37,6 +37,12 @@ def main():
         arv.Pcg32Stream(42, 0).sample(t, n, out=buf[:n])           # v8
         arv.Pcg32Stream(42, 0).sample(t, n - 4, out=buf[4:n])      # v4 (16-byte aligned)
         arv.Pcg32Stream(42, 0).sample(t, n - 1, out=buf[1:n])      # scalar stores
+    # the lane-table headline kernel (512-thread CTAs, 59 KB tables) on the same sizes and alignments
+    _native.call("arv_set_tuning", 5, 0)
+    for t in (sub, lin):
+        arv.Pcg32Stream(42, 0).sample(t, n, out=buf[:n])
+        arv.Pcg32Stream(42, 0).sample(t, n - 4, out=buf[4:n])
+    _native.call("arv_set_tuning", 5, 24)
     arv.Pcg32Stream(42, 0).sample("exact", 4096, out=buf[:4096])
     arv.Pcg32Stream(42, 0).sample_exact64(4096)
     arv.Pcg32Stream(42, 0).words(n)
@@ -46,7 +52,7 @@ def main():
     c = torch.from_numpy(np.ascontiguousarray(sub.coeffs32)).cuda()
     lat = torch.empty(1 << 23, dtype=torch.float32, device="cuda")
     fast = torch.zeros(1, dtype=torch.int32, device="cuda")
-    for mode in (0, 1):
+    for mode in (0, 1, 2):
         _native.call("arv_lattice_subdyadic_f32", c.data_ptr(), 1, 16, 3, mode, lat.data_ptr(), fast.data_ptr(),
                      dev.stream_handle())
     # drop-in kernels, device and host buffers
