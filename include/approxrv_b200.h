@@ -178,7 +178,7 @@ ARV_API int arv_store_probe_ex(float *out, int64_t n, int mode, void *stream);
 #define ARV_TUNE_GBM_KERNEL 4
 /* ARV_TUNE_LANE_MIN_N = log2 of the smallest degree-1 sub-interval call that
  * takes the lane-private-table kernel (k_pcg32_linlane: conflict-free shared
- * memory lookups, 57 KB staged per CTA); default 24; < 0: never. */
+ * memory lookups, 57 KB staged per CTA); default 26; < 0: never. */
 #define ARV_TUNE_LANE_MIN_N 5
 ARV_API int arv_set_tuning(int key, int value);
 

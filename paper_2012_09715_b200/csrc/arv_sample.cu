@@ -44,7 +44,10 @@ constexpr int kSignedUnroll = ARV_SIGNED_UNROLL;  // the signed-table generator 
 // Process-wide launch shape knobs (arv_set_tuning); defaults from sweeps.
 static int g_group = 8;        // samples per thread-group: 4 (v4) or 8 (v8)
 static int g_ctas_per_sm = 0;  // CTAs per SM (256 threads each); 0 = auto (see gen_grid)
-static int64_t g_lane_min_n = int64_t{1} << 24;  // calls of at least this many samples take the lane-table kernel (< 0: never)
+// calls of at least this many samples take the lane-table kernel (< 0: never).  Back to back
+// (tools/lane_threshold.py) it ties with the signed-table kernel at 2^22-2^23, loses 1-6% at
+// 2^24-2^25 (57 KB staged per CTA) and wins from 2^26 on (2^28: 3.6%).
+static int64_t g_lane_min_n = int64_t{1} << 26;
 extern int g_cir_segment;      // arv_mlmc.cu
 extern int g_gbm_kernel;       // arv_mlmc.cu
 
@@ -843,10 +846,10 @@ static void launch_subdyadic(uint64_t seed, uint64_t sid, uint64_t offset, const
                              float *out, int64_t n, int mode, void *stream) {
     const bool signed_tab = ARV_GEN_SIGNED && D == 1 && mode != 1 && sub_bits <= kSignedMaxBits;
     // Large calls: the lane-private table (57 KB staged per 512-thread CTA pays
-    // off from a few million samples on; g_lane_min_n, ARV_TUNE_LANE_MIN_N).
+    // off from 2^26 samples on; g_lane_min_n, ARV_TUNE_LANE_MIN_N).
     if (signed_tab && sub_bits <= kLaneMaxBits && g_lane_min_n >= 0 && n >= g_lane_min_n) {
         const void *lfn = mode == 8 ? (const void *)k_pcg32_linlane<8> : (const void *)k_pcg32_linlane<4>;
-        // per call: the attribute is per device, and a call of >= 2^24 samples does not notice it
+        // per call: the attribute is per device, and a call of >= 2^26 samples does not notice it
         cudaFuncSetAttribute(lfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kLaneBytes);
         // one wave of 3 CTAs per SM: 174.3 us vs 175.5 us for 5/3 waves at 2^28 (tools/gen_tune_lane.py)
         const int grid = gen_grid(lfn, n, mode, kLaneBytes, kLaneBlock, false);

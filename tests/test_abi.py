@@ -85,7 +85,7 @@ class TestValidationBeforeCuda:
             nat.call("arv_set_tuning", 1, 5)
         with pytest.raises(errors.ConfigError, match="lane_min_n"):
             nat.call("arv_set_tuning", 5, 41)
-        nat.call("arv_set_tuning", 5, 24)
+        nat.call("arv_set_tuning", 5, 26)
         assert nat.launch_count() == 0
 
     def test_zero_length_is_a_noop(self, nat):

@@ -53,9 +53,12 @@ def test_generator_calls_replay_from_a_graph(orc):
 
 
 def test_lane_table_kernel_replays_from_a_graph(orc):
-    """A call large enough for the lane-table headline kernel (>= 2^24 samples,
-    59 KB of opted-in dynamic shared memory) captures and replays as well."""
+    """A call through the lane-table headline kernel (59 KB of opted-in dynamic
+    shared memory, set per call) captures and replays as well."""
     import paper_2012_09715_b200 as arv
+    from paper_2012_09715_b200._native import call
+
+    call("arv_set_tuning", 5, 24)  # ARV_TUNE_LANE_MIN_N: lane-table kernel from 2^24 samples (default 2^26)
 
     sub = arv.load_table("subdyadic_linear_k16_s8")
     n = (1 << 24) + 16
@@ -78,6 +81,7 @@ def test_lane_table_kernel_replays_from_a_graph(orc):
         for lo in (0, n - m):
             want = orc.pcg32_subdyadic_f32(42, 3, i * n + lo, sub.coeffs32, sub.sub_bits, m)
             assert np.array_equal(bits(out[i, lo:lo + m]), want.view(np.uint32)), (i, lo)
+    call("arv_set_tuning", 5, 26)
 
 
 def test_dropin_eval_replays_from_a_graph(orc, tables_npz):

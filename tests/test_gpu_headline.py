@@ -133,14 +133,14 @@ import contextlib
 @contextlib.contextmanager
 def lane_min_n(log2n):
     """ARV_TUNE_LANE_MIN_N (key 5): calls of >= 2^log2n samples take the
-    lane-table kernel (default 24); < 0 never."""
+    lane-table kernel (default 26); < 0 never."""
     from paper_2012_09715_b200._native import call
 
     call("arv_set_tuning", 5, log2n)
     try:
         yield
     finally:
-        call("arv_set_tuning", 5, 24)
+        call("arv_set_tuning", 5, 26)
 
 
 def _subtable(arv, c, b):
@@ -216,7 +216,7 @@ def test_pdl_table_written_by_previous_kernel(arv, orc, tables_npz):
         big = torch.empty(1 << 26, dtype=torch.float32, device="cuda")
         call("arv_store_probe", big.data_ptr(), big.numel(), s)
         ref = orc.pcg32_subdyadic_f32(42, 0, 0, (base * np.float32(scale)).astype(np.float32), 3, n)
-        for lm in (24, 0):  # signed-table kernel, lane-table kernel
+        for lm in (26, 0):  # signed-table kernel, lane-table kernel
             c.zero_()
             call("arv_store_probe", big.data_ptr(), big.numel(), s)
             torch.mul(src, scale, out=c)

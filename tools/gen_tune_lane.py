@@ -1,6 +1,6 @@
 """Headline generator: signed-table kernel vs lane-table kernel (ARV_TUNE_LANE_MIN_N).
 
-    python tools/gen_tune_lane.py <lane_min_n_log2: -1 = signed kernel, 24 = lane kernel> [ctas_per_sm]
+    python tools/gen_tune_lane.py <lane_min_n_log2: -1 = signed kernel, 24 / 26 = lane kernel> [ctas_per_sm]
 
 One variant per process, so that the burst figure (200 back-to-back 2^28
 launches from an idle GPU, as bench.py) is not taken at the power cap the

@@ -42,7 +42,7 @@ def main():
     for t in (sub, lin):
         arv.Pcg32Stream(42, 0).sample(t, n, out=buf[:n])
         arv.Pcg32Stream(42, 0).sample(t, n - 4, out=buf[4:n])
-    _native.call("arv_set_tuning", 5, 24)
+    _native.call("arv_set_tuning", 5, 26)
     arv.Pcg32Stream(42, 0).sample("exact", 4096, out=buf[:4096])
     arv.Pcg32Stream(42, 0).sample_exact64(4096)
     arv.Pcg32Stream(42, 0).words(n)
