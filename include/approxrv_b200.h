@@ -180,6 +180,10 @@ ARV_API int arv_store_probe_ex(float *out, int64_t n, int mode, void *stream);
  * takes the lane-private-table kernel (k_pcg32_linlane: conflict-free shared
  * memory lookups, 57 KB staged per CTA); default 26; < 0: never. */
 #define ARV_TUNE_LANE_MIN_N 5
+/* ARV_TUNE_NC_CERTIFY = 1 (default): warm-started bulk ncchi2 quantile solves may skip
+ * the verification sweep when the Taylor polynomial's last terms certify the step
+ * (csrc/arv_ncchi2.cuh); 0: every step is verified by a second CDF sweep. */
+#define ARV_TUNE_NC_CERTIFY 6
 ARV_API int arv_set_tuning(int key, int value);
 
 /* ---- nested MLMC level kernels ------------------------------------------
@@ -266,6 +270,10 @@ ARV_API int arv_ncchi2_inv_cdf_tol(const double *u, const double *lam, int64_t n
 /* Device non-central chi^2 CDF (Poisson-mixture of regularized gammas). */
 ARV_API int arv_ncchi2_cdf(const double *x, const double *lam, int64_t nlam, double nu, double *out, int64_t n,
                    void *stream);
+/* Number of quantile solves (arv_ncchi2_inv_cdf*, the CIR exact level kernels) that took
+ * the certified single-sweep shortcut (ARV_TUNE_NC_CERTIFY) since the last call; resets it.
+ * Synchronises the device. */
+ARV_API int arv_nc_certified_count(unsigned long long *out);
 /* Test hook: out[i] = the exact-side standard normal the Gaussian MLMC level
  * kernels compute for the 32-bit word words[i] (u = (w + 1/2) 2^-32): AS241
  * (exact_dist.py:65-126) with fused multiply-adds, a reciprocal-based

@@ -79,6 +79,7 @@ _SIGNATURES = {
     "arv_ncchi2_inv_cdf": ([_p, _p, _i64, _dbl, _p, _p, _p, _i64, _p], _int),
     "arv_ncchi2_inv_cdf_tol": ([_p, _p, _i64, _dbl, _p, _dbl, _p, _p, _i64, _p], _int),
     "arv_ncchi2_cdf": ([_p, _p, _i64, _dbl, _p, _i64, _p], _int),
+    "arv_nc_certified_count": ([_p], _int),
     "arv_test_level_normals": ([_p, _p, _i64, _p], _int),
 }
 

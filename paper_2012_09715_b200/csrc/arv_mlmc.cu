@@ -1615,6 +1615,14 @@ struct CirWs {
 
 }  // namespace arv
 
+namespace arv {
+int set_nc_certify(int on) {
+    const int v = on ? 1 : 0;
+    cudaMemcpyToSymbol(g_nc_certify_on, &v, sizeof v);
+    return check_launch("arv_set_tuning(ARV_TUNE_NC_CERTIFY)");
+}
+}  // namespace arv
+
 using namespace arv;
 
 extern "C" {
@@ -1854,6 +1862,15 @@ int arv_test_level_normals(const uint32_t *words, double *out, int64_t n, void *
     k_level_normals<<<stream_grid(n, 256, 8), 256, 0, as_stream(stream)>>>(words, out, n);
     note_launch();
     return check_launch("arv_test_level_normals");
+}
+
+// Quantile solves that took the certified single-sweep shortcut since the last call (and reset).
+ARV_API int arv_nc_certified_count(unsigned long long *out) {
+    if (!out) return set_error(ARV_ERR_CONFIG, "arv_nc_certified_count: null output");
+    cudaMemcpyFromSymbol(out, g_nc_certified, sizeof(unsigned long long));
+    const unsigned long long zero = 0;
+    cudaMemcpyToSymbol(g_nc_certified, &zero, sizeof zero);
+    return check_launch("arv_nc_certified_count");
 }
 
 #if ARV_NC_COUNT

@@ -164,8 +164,9 @@ __device__ inline NcLam nc_lam(double lam, double sigmas = kNcSigmas) {
 // window drops < 1e-15 of the Poisson mass, and the downward recurrence
 // drifts by ~(window length) ulp, so F moves by < 1e-13 and one FP64
 // operation per term is saved.
-template <bool FULL, bool NARROW = false>
-__device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, double u, double &inv_w) {
+template <bool FULL>
+__device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, double u, double &inv_w,
+                                         const bool NARROW = false) {
     const double y = 0.5 * x;
     const int top = NARROW ? L.top_n : L.top, bot = NARROW ? L.bot_n : L.bot;
     const float sig = NARROW ? static_cast<float>(kNcSigmasStart) : static_cast<float>(L.sigmas);
@@ -204,7 +205,7 @@ __device__ inline NcCdf ncchi2_cdf_sweep(double a0, double x, const NcLam &L, do
     if (L.h > 0.0) {
         const double inv_h = L.inv_h;
         double p = L.p_top;
-        if constexpr (NARROW) {  // Poisson weight at the narrow window top
+        if (NARROW) {  // Poisson weight at the narrow window top
             for (int i = L.top; i > top; --i) p *= static_cast<double>(i) * inv_h;
         }
         double acc = 0.0, dens = 0.0, s0 = 0.0;
@@ -294,8 +295,12 @@ struct NcQuantile {
 // (start + verification) instead of the 2.98 of Newton / Halley steps
 // (tools/nc_diag.py).  DEG 4 / 5 / 6 measured 22.9 / 23.4 / 23.5 ms at
 // level 6.  Returns the x-step, or NaN.
+struct NcStep {
+    double dx;      // the x-step
+    double t1, t2;  // |c_{DEG-1} d^{DEG-1}|, |c_DEG d^DEG|: the polynomial's last two terms at the root
+};
 template <int DEG>
-__device__ inline double nc_taylor_step(const NcCdf &c, double a0, double h, double x) {
+__device__ inline NcStep nc_taylor_step_terms(const NcCdf &c, double a0, double h, double x) {
     const double inv_y = 2.0 / x;
     double D[DEG];
     double sm = c.s0, sk = 2.0 * c.pdf;  // S_{k-1}, S_k
@@ -333,13 +338,32 @@ __device__ inline double nc_taylor_step(const NcCdf &c, double a0, double h, dou
         if (it == 0) inv_dp = 1.0 / dp;
         d = fma(-p, inv_dp, d);
     }
-    return 2.0 * d;
+    double pw = d;
+#pragma unroll
+    for (int n = 2; n <= DEG - 1; ++n) pw *= d;  // d^(DEG-1)
+    return {2.0 * d, fabs(cf[DEG - 1] * pw), fabs(cf[DEG] * pw * d)};
+}
+template <int DEG>
+__device__ inline double nc_taylor_step(const NcCdf &c, double a0, double h, double x) {
+    return nc_taylor_step_terms<DEG>(c, a0, h, x).dx;  // the term sizes are dead code here
 }
 
 #if ARV_NC_COUNT  // diagnostic build: CDF evaluations per solve, per lane and per warp (max)
 __device__ unsigned long long g_nc_evals, g_nc_solves, g_nc_hist[8], g_nc_warp_hist[8];
 #endif
 
+#ifndef ARV_NC_CERTIFY
+#define ARV_NC_CERTIFY 1
+#endif
+#ifndef ARV_NC_CERT_DIV
+#define ARV_NC_CERT_DIV 8.0  // |c5 d^5| <= tol_f / this
+#endif
+// Run-time switch (arv_set_tuning(ARV_TUNE_NC_CERTIFY, 0 / 1), default on) and a
+// counter of solves that took the certified shortcut (arv_nc_certified_count:
+// the tests assert that the shortcut actually ran where it should).
+__device__ int g_nc_certify_on = 1;
+__device__ unsigned long long g_nc_certified = 0;
+constexpr double kNcCertifyMinTail = 1e-3;  // certified shortcut only for min(u, 1 - u) >= this (tol_f = 1e-9 there)
 // exact_dist.py:381-461 contract, per element, warm start x0 (<= 0: mean);
 // tol is the reference's `tol` argument (default 1e-9).  Same bracket,
 // tolerance and 1e-8 residual contract as _vector_newton: each step is the
@@ -357,44 +381,85 @@ __device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, do
     x = fmin(fmax(x, 1e-8), hi);
     const NcLam L = nc_lam(lam, fmin(u, one_minus_u) >= 1e-6 ? kNcSigmasBulk : kNcSigmas);
     double inv_w;
-    // bulk solves: the first sweep only places the Taylor step (6-sigma window);
-    // the verification and any further sweeps use the full window
-    const bool narrow = L.blocked && ARV_NC_NARROW_START;
-    NcCdf c = narrow ? ncchi2_cdf_sweep<true, true>(a0, x, L, u, inv_w) : ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w);
-    if (narrow && fabs(c.resid) <= tol_f) {
-        // The narrow window truncates ~1e-11..1e-10, about tol_f: never accept
-        // (or bracket on) its residual -- re-evaluate on the full window.
-        const NcCdf f = ncchi2_cdf_sweep<false>(a0, x, L, u, inv_w);
-        c = fabs(f.resid) <= tol_f ? f : ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w);
-    }
-#if ARV_NC_COUNT
-    int n_eval = 1;
-#endif
-    for (int it = 0; it < 80; ++it) {
-        if (fabs(c.resid) <= tol_f) break;
+    // Certified single-sweep solve (bulk quantiles from a warm start).  One
+    // full-width sweep gives F, S_0, S_1 at the warm start to ~1e-12; the root d
+    // of the degree-6 Taylor polynomial of F is accepted WITHOUT the
+    // verification sweep when the polynomial's terms at d decay at least
+    // geometrically by 1/4 (|c6 d^6| <= |c5 d^5| / 4, so the omitted terms are
+    // bounded by about |c6 d^6| / 3) and its last two terms are far below the
+    // tolerance (|c5 d^5| <= tol_f / 8: the residual is then below ~tol_f / 24).  A warp takes the shortcut only if
+    // all of its lanes certify (the others would make it run the verification
+    // sweep anyway, and then every lane is verified for free).  Lanes that do
+    // not qualify -- larger warm-start errors, tails, no warm start -- take the
+    // verified path unchanged.  tests/test_gpu_mlmc.py checks the shortcut's
+    // residuals against the 8-sigma CDF entry point.
+    const bool candidate = ARV_NC_CERTIFY && g_nc_certify_on && x0 > 0.0 && L.blocked &&
+                           fmin(u, one_minus_u) >= kNcCertifyMinTail;
+    // other bulk solves: the first sweep only places the Taylor step (6-sigma
+    // window); the verification and any further sweeps use the full window
+    bool narrow = L.blocked && ARV_NC_NARROW_START && !candidate;
+    // One loop, one call site per sweep kind (the sweeps are large: every
+    // inlined copy costs instruction cache).  `full`: evaluate F with S_0, S_1
+    // at x, else F only (the verification of a step).
+    bool full = true, first = true;
+    NcCdf c = {0.0, 0.0, 0.0};
+    int n_eval = 0;
+    (void)n_eval;  // read by the ARV_NC_COUNT build only
+    for (int it = 0; it < 200; ++it) {
+        if (full) {
+            c = ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w, narrow);
+        } else {
+            const NcCdf f = ncchi2_cdf_sweep<false>(a0, x, L, u, inv_w);
+            c.resid = f.resid;
+        }
+        ++n_eval;
+        if (!full) {  // a verification: accept, or get the derivatives at this point for another step
+            if (fabs(c.resid) <= tol_f) break;
+            full = true;
+            continue;
+        }
+        if (fabs(c.resid) <= tol_f) {
+            if (!narrow) break;
+            // The narrow window truncates ~1e-11..1e-10, about tol_f: never accept
+            // (or bracket on) its residual -- re-evaluate on the full window.
+            narrow = false;
+            full = false;
+            continue;
+        }
+        narrow = false;
+        if (!first && hi - lo < 1e-15 * hi) break;
         if (c.resid > 0.0) hi = x;
         else lo = x;
+        double dx;
+        bool certified = false;
+        if (first && candidate) {
+            const NcStep st = nc_taylor_step_terms<6>(c, a0, L.h, x);
+            dx = -st.dx;
+            certified = isfinite(dx) && x - dx > lo && x - dx < hi && st.t1 <= tol_f * (1.0 / ARV_NC_CERT_DIV) &&
+                        st.t2 <= 0.25 * st.t1 && fabs(dx) <= 0.05 * x;
+            c.resid = certified ? st.t1 + st.t2 : c.resid;
+        } else {
 #if ARV_NC_TAYLOR
-        double dx = -nc_taylor_step<ARV_NC_TAYLOR>(c, a0, L.h, x);
-        if (!isfinite(dx)) dx = c.resid / c.pdf;  // Newton
+            dx = -nc_taylor_step<ARV_NC_TAYLOR>(c, a0, L.h, x);
 #else
-        double dx = c.resid / c.pdf;  // Newton
+            dx = c.resid / c.pdf;
 #endif
+        }
+        if (!isfinite(dx)) dx = c.resid / c.pdf;  // Newton
         double xn = x - dx;
         if (!isfinite(xn) || xn <= lo || xn >= hi) xn = 0.5 * (lo + hi);
         x = xn;
-#if ARV_NC_TAYLOR
+        if (first && candidate) {
+            const unsigned am = __activemask();
+            if (__all_sync(am, certified)) {  // c.resid = the term estimate
+                if ((threadIdx.x & 31) == __ffs(am) - 1) atomicAdd(&g_nc_certified, static_cast<unsigned long long>(__popc(am)));
+                break;
+            }
+        }
+        first = false;
         // Verify the step with the F-only sweep; only a failed step (0.01%
         // of solves) needs the derivatives at the new point for another one.
-        c = ncchi2_cdf_sweep<false>(a0, x, L, u, inv_w);
-        if (fabs(c.resid) > tol_f) c = ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w);
-#else
-        c = ncchi2_cdf_sweep<true>(a0, x, L, u, inv_w);
-#endif
-#if ARV_NC_COUNT
-        ++n_eval;
-#endif
-        if (hi - lo < 1e-15 * hi) break;
+        full = ARV_NC_TAYLOR ? false : true;
     }
 #if ARV_NC_COUNT
     atomicAdd(&g_nc_evals, static_cast<unsigned long long>(n_eval));

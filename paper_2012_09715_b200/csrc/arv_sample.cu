@@ -50,6 +50,7 @@ static int g_ctas_per_sm = 0;  // CTAs per SM (256 threads each); 0 = auto (see 
 static int64_t g_lane_min_n = int64_t{1} << 26;
 extern int g_cir_segment;      // arv_mlmc.cu
 extern int g_gbm_kernel;       // arv_mlmc.cu
+int set_nc_certify(int on);    // arv_mlmc.cu
 
 constexpr int kJumpBits = 24;  // grid threads < 2^24
 
@@ -934,6 +935,8 @@ int arv_set_tuning(int key, int value) {
             if (value > 40) return set_error(ARV_ERR_CONFIG, "lane_min_n (log2) must be <= 40");
             g_lane_min_n = value < 0 ? -1 : (int64_t{1} << value);
             return ARV_OK;
+        case ARV_TUNE_NC_CERTIFY:
+            return set_nc_certify(value);
         case ARV_TUNE_CTAS_PER_SM:
             if (value < 0 || value > 32) return set_error(ARV_ERR_CONFIG, "ctas_per_sm must be in [0 (auto), 32]");
             g_ctas_per_sm = value;

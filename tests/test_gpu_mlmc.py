@@ -136,6 +136,99 @@ def test_device_ncchi2_cdf_accuracy(arv, nu):
         assert err.max() <= 1e-12, (lam, err.max(), x[np.argmax(err)])
 
 
+def _certified_count():
+    import ctypes
+
+    from paper_2012_09715_b200._native import call
+
+    c = ctypes.c_ulonglong(0)
+    call("arv_nc_certified_count", ctypes.byref(c))
+    return int(c.value)
+
+
+@pytest.mark.parametrize("nu", [4 * 0.5 * 0.04 / 0.2**2, 1.0, 7.3])
+def test_certified_single_sweep_quantile_residuals(arv, nu):
+    """A warm-started bulk solve may return the root of the degree-6 Taylor
+    polynomial of its one CDF sweep WITHOUT a verification sweep, when the
+    polynomial's last terms certify it (arv_ncchi2.cuh, ARV_TUNE_NC_CERTIFY).
+    The contract is unchanged: |F(x) - u| <= tol_f = 1e-9 in the bulk.  Checked
+    with the independent 8-sigma CDF entry point on 2^21 solves per warm-start
+    class -- lambda from 0 to 600 plus a fine grid of small lambda, u over
+    (1e-3, 1 - 1e-3), warm starts off by relative 1e-4 ... 5e-2 (the tables'
+    error is ~1e-3) -- with the shortcut's use counted, and against the same
+    solves with the shortcut switched off."""
+    from paper_2012_09715_b200 import _device as dev
+    from paper_2012_09715_b200 import exact_dist
+    from paper_2012_09715_b200._native import call
+
+    n = 1 << 21
+    g = torch.Generator(device="cuda").manual_seed(12345)
+
+    def rand(m=n):
+        return torch.rand(m, dtype=torch.float64, device="cuda", generator=g)
+
+    u = rand() * (1 - 2e-3) + 1e-3
+    lam = rand() * 600.0
+    lam[n // 2: 3 * n // 4] = rand(n // 4) ** 3 * 8.0  # small lambda
+    lam[:1024] = 0.0
+    lam, _ = torch.sort(lam)  # warps of similar lambda, as the bucketed CIR level kernels have them
+    _certified_count()  # reset
+    x_ref = exact_dist.ncchi2_inv_cdf_batch(u, nu, lam)  # no warm start: the verified path
+    assert _certified_count() == 0
+
+    def residual(x):
+        out = torch.empty_like(x)
+        call("arv_ncchi2_cdf", x.data_ptr(), lam.data_ptr(), n, nu, out.data_ptr(), n, dev.stream_handle())
+        return (out - u).abs()
+
+    assert float(residual(x_ref).max()) <= 1.01e-9
+    for eps, min_share in ((1e-4, 0.5), (1e-3, 0.5), (3e-3, 0.2), (1e-2, 0.0), (5e-2, 0.0)):
+        x0 = x_ref * (1 + eps * (2 * rand() - 1))
+        x = exact_dist.ncchi2_inv_cdf_batch(u, nu, lam, x0=x0)
+        share = _certified_count() / n
+        r = residual(x)
+        k = int(torch.argmax(r))
+        assert float(r[k]) <= 1.01e-9, (eps, float(r[k]), float(u[k]), float(lam[k]), float(x0[k]))
+        assert share >= min_share, (eps, share)
+        if eps == 3e-3:  # no start is within tolerance by luck here: every solve stepped, ~60% unverified
+            assert float(r[k]) <= 1e-10, float(r[k])
+        call("arv_set_tuning", 6, 0)  # ARV_TUNE_NC_CERTIFY off: every step verified
+        try:
+            xv = exact_dist.ncchi2_inv_cdf_batch(u, nu, lam, x0=x0)
+        finally:
+            call("arv_set_tuning", 6, 1)
+        assert _certified_count() == 0
+        # both solve F(x) = u to 1e-9: they differ by at most 2e-9 / f(x)
+        assert float(((x - xv).abs() / xv).max()) <= 1e-6
+        print(f"nu={nu:.4g} eps={eps:g}: {100 * share:.1f}% of solves certified, max residual {float(r[k]):.3g}")
+
+
+def test_certified_shortcut_from_the_cir_table_warm_start(arv):
+    """The CIR level kernels' own warm start (the 64-knot table): residuals of
+    the device quantile against the 8-sigma CDF, bulk and both tails."""
+    from paper_2012_09715_b200 import _device as dev
+    from paper_2012_09715_b200 import _kernels, exact_dist
+    from paper_2012_09715_b200._native import call
+
+    tab = arv.load_table("ncchi2_cir_k64_stacks")
+    n = 1 << 21
+    g = torch.Generator(device="cuda").manual_seed(7)
+    u = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * (1 - 2e-6) + 1e-6
+    lam, _ = torch.sort(torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 500.0)
+    x0 = torch.empty_like(u)
+    _kernels.ncchi2_eval(tab.eval_stacks, tab.nu, u, lam, x0)
+    _certified_count()
+    x = exact_dist.ncchi2_inv_cdf_batch(u, tab.nu, lam, x0=x0.clamp_min(1e-12))
+    share = _certified_count() / n
+    out = torch.empty_like(x)
+    call("arv_ncchi2_cdf", x.data_ptr(), lam.data_ptr(), n, tab.nu, out.data_ptr(), n, dev.stream_handle())
+    tol_f = torch.clamp(1e-4 * torch.minimum(u, 1 - u), min=1e-13, max=1e-9)
+    r = (out - u).abs()
+    assert bool((r <= tol_f * 1.01 + 2e-12).all()), float((r / tol_f).max())
+    assert share >= 0.3, share
+    print(f"table warm start: {100 * share:.1f}% of solves certified, max residual {float(r.max()):.3g}")
+
+
 def test_level_stats_match_per_path(arv):
     lin = arv.load_table("dyadic_linear_k15")
     spec = arv.LevelSpec(level=3, scheme="euler_maruyama", process=arv.GbmParams(**GBM), rv_source=lin,
