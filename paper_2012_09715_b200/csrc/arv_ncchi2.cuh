@@ -363,7 +363,7 @@ __device__ unsigned long long g_nc_evals, g_nc_solves, g_nc_hist[8], g_nc_warp_h
 // the tests assert that the shortcut actually ran where it should).
 __device__ int g_nc_certify_on = 1;
 __device__ unsigned long long g_nc_certified = 0;
-constexpr double kNcCertifyMinTail = 1e-3;  // certified shortcut only for min(u, 1 - u) >= this (tol_f = 1e-9 there)
+constexpr double kNcCertifyMinTail = 1e-5;  // certified shortcut only for min(u, 1 - u) >= this (tol_f = 1e-9 there)
 // exact_dist.py:381-461 contract, per element, warm start x0 (<= 0: mean);
 // tol is the reference's `tol` argument (default 1e-9).  Same bracket,
 // tolerance and 1e-8 residual contract as _vector_newton: each step is the
