@@ -369,8 +369,9 @@ constexpr double kNcCertifyMinTail = 1e-5;  // certified shortcut only for min(u
 // tolerance and 1e-8 residual contract as _vector_newton: each step is the
 // Taylor-polynomial root (nc_taylor_step; plain Newton if it is not finite),
 // which the bracket safeguard accepts or replaces by bisection.  From the
-// table warm start 99.99% of solves finish after the start sweep and one
-// verification sweep (tools/nc_diag.py).
+// table warm start 99.9% of bulk solves are certified after the start sweep
+// alone (below); the others finish after one verification sweep
+// (tools/nc_diag.py).
 __device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, double x0, double tol = 1e-9) {
     const double a0 = 0.5 * nu;
     const double one_minus_u = 1.0 - u;
