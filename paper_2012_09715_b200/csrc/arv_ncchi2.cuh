@@ -38,6 +38,12 @@
 
 #include "arv_common.cuh"
 
+#include "arv_logtab.cuh"
+
+#ifndef ARV_NC_FAST_LOG
+#define ARV_NC_FAST_LOG 1
+#endif
+
 namespace arv {
 
 // stirlerr(n) = log Gamma(n + 1) - (n + 1/2) log n + n - log sqrt(2 pi):
@@ -50,6 +56,30 @@ static __constant__ double kStirlerrInt[16] = {
     2.0790672103765093e-2, 1.6644691189821192e-2, 1.3876128823070748e-2, 1.1896709945891770e-2,
     1.0411265261972096e-2, 9.2554621827127329e-3, 8.3305634333628713e-3, 7.5736754879518408e-3,
     6.9428401072095299e-3, 6.4089941880042071e-3, 5.9513701127588477e-3, 5.5547335519628014e-3};
+
+// log(x) for a positive normal x from the level kernels' 128-bucket table
+// (arv_logtab.cuh; the same evaluation as g2::neg_log in arv_mlmc.cu): 9 FP64
+// operations where CUDA's log() takes ~25 plus ~30 other instructions.
+// Absolute error ~2^-58 + 1.1 ulp of the result; its uses here are
+// log(2 pi x) with x >= 1 and log(x / m) with |log| >= 0.2.
+__device__ __forceinline__ double nc_log(double v) {
+#if ARV_NC_FAST_LOG
+    const int hi = __double2hiint(v);
+    if (static_cast<unsigned>(hi - 0x00100000) >= 0x7FE00000u) return log(v);  // zero, subnormal, negative, inf, nan
+    const int ne = 1023 - (hi >> 20);
+    const double2 tj = __ldg(kLogTab + ((hi >> 13) & 127));
+    const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, __double2loint(v));
+    const double r = fma(m, tj.x, -1.0);
+    double q = fma(r, -1.0 / 6.0, 0.2);
+    q = fma(q, r, -0.25);
+    q = fma(q, r, 1.0 / 3.0);
+    q = fma(q, r, -0.5);
+    const double lp = fma(r * r, q, r);
+    return lp - fma(static_cast<double>(ne), 0.6931471805599453094, tj.y);
+#else
+    return log(v);
+#endif
+}
 
 __device__ inline double nc_stirlerr(double n) {
     if (n <= 15.0 && n == floor(n)) return kStirlerrInt[static_cast<int>(n)];
@@ -79,7 +109,7 @@ __device__ inline double nc_bd0(double x, double m) {
         t = fma(t, v2, 1.0 / 3.0);
         return fma(2.0 * x * v, v2 * t, d * v);
     }
-    return x * log(x / m) + m - x;
+    return x * nc_log(x / m) + m - x;
 }
 
 // log(m^x e^-m / Gamma(x + 1)) for real x >= 0, m >= 0
@@ -87,7 +117,7 @@ __device__ inline double nc_logdens(double x, double m) {
     if (m <= 0.0) return x == 0.0 ? 0.0 : -INFINITY;
     if (x == 0.0) return -m;
     constexpr double kTwoPi = 6.283185307179586476925286766559;
-    return -nc_stirlerr(x) - nc_bd0(x, m) - 0.5 * log(kTwoPi * x);
+    return -nc_stirlerr(x) - nc_bd0(x, m) - 0.5 * nc_log(kTwoPi * x);
 }
 
 struct NcCdf {
