@@ -1684,7 +1684,10 @@ int arv_mlmc_gaussian_level(const arv_level_spec *spec, const double *coeffs, in
     const size_t smem2 = sizeof(double) * (degree == 0 ? 1 : ((degree + 2) & ~1)) * K1;
     // v3 (phased exact side): both sides wanted, PCG32; the table + the block buffers
     const size_t smem3 = v3_smem_bytes(degree, K1);
-    const int kern = g_gbm_kernel ? g_gbm_kernel : (ARV_GBM_V3 ? 3 : 2);
+    // auto: the phased kernel from 8 fine steps per path on; below that its per-block machinery (two
+    // barriers, the CTA-wide tail list) costs more than it saves (levels 0 / 1 / 2 of config 4: 0.101 /
+    // 0.116 / 0.142 ms with v2 against 0.121 / 0.129 / 0.152 ms; level 3 ties).  Same results bit for bit.
+    const int kern = g_gbm_kernel ? g_gbm_kernel : (ARV_GBM_V3 && A.n_f >= 8 ? 3 : 2);
     const bool use_v3 = kern == 3 && A.rng == ARV_RNG_PCG32 && A.want_exact && A.want_approx &&
                         smem3 <= 96 * 1024;
     cudaStream_t s = as_stream(stream);
