@@ -470,7 +470,8 @@ __device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, do
         if (first && candidate) {
             const NcStep st = nc_taylor_step_terms<6>(c, a0, L.h, x);
             dx = -st.dx;
-            certified = isfinite(dx) && x - dx > lo && x - dx < hi && fmax(st.t1, st.t2) <= tol_f * (1.0 / ARV_NC_CERT_DIV) && fabs(dx) <= 0.05 * x;
+            certified = isfinite(dx) && x - dx > lo && x - dx < hi && fabs(dx) <= 0.05 * x &&
+                        fmax(st.t1, st.t2) <= tol_f * (1.0 / ARV_NC_CERT_DIV);
             c.resid = certified ? st.t1 + st.t2 : c.resid;
         } else {
 #if ARV_NC_TAYLOR
@@ -486,7 +487,8 @@ __device__ inline NcQuantile ncchi2_quantile(double u, double nu, double lam, do
         if (first && candidate) {
             const unsigned am = __activemask();
             if (__all_sync(am, certified)) {  // c.resid = the term estimate
-                if ((threadIdx.x & 31) == __ffs(am) - 1) atomicAdd(&g_nc_certified, static_cast<unsigned long long>(__popc(am)));
+                if ((threadIdx.x & 31) == __ffs(am) - 1)
+                    atomicAdd(&g_nc_certified, static_cast<unsigned long long>(__popc(am)));
                 break;
             }
         }
