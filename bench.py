@@ -18,6 +18,7 @@ sub-intervals), all host threads, bounded samples per step.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -696,6 +697,8 @@ def mlmc_metrics(arv, args, rank, world, device) -> dict:
     included), max over ranks."""
     import torch
 
+    from paper_2012_09715_b200 import _native
+
     group = None
     if world > 1:
         import torch.distributed as dist
@@ -716,6 +719,9 @@ def mlmc_metrics(arv, args, rank, world, device) -> dict:
         arv.estimate_level_suites(specs, streams, n_paths, group=group)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        certified = ctypes.c_ulonglong(0)
+        if scheme == "cir_exact":
+            _native.call("arv_nc_certified_count", ctypes.byref(certified))  # reset (outside the timed region)
         e0.record()
         # raises NumericalError if any rank's exact transitions failed
         suites = arv.estimate_level_suites(specs, streams, n_paths, group=group)
@@ -736,6 +742,10 @@ def mlmc_metrics(arv, args, rank, world, device) -> dict:
                                            n_paths * steps / secs)
         if scheme == "cir_exact":
             entry["n_fail"] = 0
+            # exact transitions solved with one CDF sweep (certified Taylor root, csrc/arv_ncchi2.cuh)
+            _native.call("arv_nc_certified_count", ctypes.byref(certified))
+            my_paths = suites[0][next(iter(suites[0]))].n_paths // max(world, 1)
+            entry["single_sweep_solves_share"] = int(certified.value) / max(my_paths * steps, 1)
             entry["log2_correction_gap"] = [float(np.log2(s["correction"].variance / s["plain_exact"].variance))
                                             for s in suites]
             entry["process_variance"] = [s["plain_exact"].variance for s in suites]
