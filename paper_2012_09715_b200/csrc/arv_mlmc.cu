@@ -50,7 +50,8 @@ constexpr int kMinLevelBlock = kCirBlock < kLevelBlock ? kCirBlock : kLevelBlock
 #define ARV_GBM_MINB 3
 #endif
 #ifndef ARV_CIR_MINB
-#define ARV_CIR_MINB 4  // 64 registers (24 B spill) -> 4 CTAs/SM: 57.4 vs 60.6 ms at 3, 60.1 at 5
+#define ARV_CIR_MINB 3  // 80 registers, no spill: level 6 10.72 ms vs 11.10 at 4 (64 registers, 56 B spilled) and 11.28 at 5
+                        // with the single-loop quantile solver; the round-1 solver preferred 4 (57.4 vs 60.6 ms)
 #endif
 constexpr int kFinalBlock = 1024;
 
